@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark of the decentralized feedforward equalization path on B200.
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted on):
+cfg2 = PD L-MMSE, B=128 antennas in C=4 clusters of 32, U=16 UEs, 16-QAM,
+W=1200 subcarriers x T=14 OFDM symbols, SNR 0..20 dB in 2 dB steps.  One
+step = one pass of the hot path over one batch: the 11 frames (one per SNR
+point) = 13,200 (subcarrier, frame) items x 14 symbols, in ONE fused kernel
+launch (Gram + matched filter + regularized Cholesky solve + unbiasing +
+hard demap).
+
+metric: detected Gb/s = frames x W x T x U x log2(M) / device time.
+Prints ONE JSON line (rank 0).  --impl reference times the reference
+algorithm's CPU implementation (the oracle port, oracle/dbp_oracle.py) on all
+host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    # name: arch, kind, B, C, U, bits, snr list (one frame per entry), frames, t_max
+    "cfg1": dict(arch="fd", kind="lmmse", B=64, C=2, U=8, bits=4, snr=[10.0], frames=1, t_max=0),
+    "cfg2": dict(arch="pd", kind="lmmse", B=128, C=4, U=16, bits=4, snr=[float(s) for s in range(0, 21, 2)],
+                 frames=11, t_max=0),
+    "cfg3-zf": dict(arch="fd", kind="zf", B=256, C=8, U=16, bits=6, snr=[15.0], frames=1, t_max=0),
+    "cfg3-mrc": dict(arch="fd", kind="mrc", B=256, C=8, U=16, bits=6, snr=[15.0], frames=1, t_max=0),
+    "cfg4-fd": dict(arch="fd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=1, t_max=10),
+    "cfg4-pd": dict(arch="pd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=1, t_max=10),
+    "cfg5-pd512": dict(arch="pd", kind="lmmse", B=512, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
+    "cfg5-fd512": dict(arch="fd", kind="lmmse", B=512, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
+    "cfg5-pd1024": dict(arch="pd", kind="lmmse", B=1024, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
+    "cfg5-fd1024": dict(arch="fd", kind="lmmse", B=1024, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
+}
+W, T = 1200, 14
+CONST = {2: "qpsk", 4: "qam16", 6: "qam64"}
+METRIC = "detected Gb/s (device-timed, max over ranks)"
+L2_BYTES = 126 * 2 ** 20
+
+
+def wl_desc(name, wl):
+    return (f"{name}: {wl['arch'].upper()} {wl['kind']} B={wl['B']} C={wl['C']} Bc={wl['B'] // wl['C']} "
+            f"U={wl['U']} {CONST[wl['bits']]} W={W} T={T} frames/step={wl['frames']}")
+
+
+def bits_per_step(wl):
+    return wl["frames"] * W * T * wl["U"] * wl["bits"]
+
+
+def algorithmic_bytes(wl, items):
+    """H + Y read once, outputs written once (xhat c64, sigma2 f32, dec u8,
+    status i32, nu f32 for FD) -- SURVEY.md 8(d)."""
+    b, u = wl["B"], wl["U"]
+    lama = wl["kind"] == "lama"
+    wdim = T if lama else u
+    per = 8 * b * u + 8 * T * b + 8 * T * u + 4 * wdim + T * u + 4
+    if wl["arch"] == "fd":
+        per += 4 * wl["C"] * wdim
+    return per * items
+
+
+# --------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """NVML sampler (SM clock, throttle reasons) running during the timed
+    region."""
+
+    def __init__(self, device_index=0, period=0.01):
+        self.samples = []
+        self.reasons = set()
+        self.ok = False
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------- CPU oracle ----
+def _cpu_worker(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, REPO)
+    import numpy as _np
+
+    from oracle import dbp_oracle as O
+
+    arch, kind, H, Y, n0s, offsets, bits, t_max = args
+    syms, _ = O.square_qam(bits)
+    lp = {"t_max": t_max} if kind == "lama" else None
+    fn = O.fd_equalize if arch == "fd" else O.pd_equalize
+    count = 0
+    for n in range(H.shape[0]):
+        h = H[n].astype(_np.complex128)
+        for t in range(Y.shape[1]):
+            r = fn(kind, h, Y[n, t].astype(_np.complex128), offsets, float(n0s[n]), 1.0, syms, lp)
+            O.hard_detect_index(r["z"], syms)
+            count += 1
+    return count
+
+
+class CpuBaseline:
+    """The reference path per vector (as montecarlo._equalize drives it),
+    restated in oracle/dbp_oracle.py, over a process pool with one BLAS thread
+    per worker."""
+
+    def __init__(self, wl, H, Y, n0_items):
+        import multiprocessing as mp
+
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.cores = os.cpu_count() or 1
+        self.pool = mp.get_context("spawn").Pool(self.cores)
+        self.wl = wl
+        self.H, self.Y, self.n0 = H, Y, n0_items
+        self.offsets = [i * (wl["B"] // wl["C"]) for i in range(wl["C"] + 1)]
+        # calibrate: vectors per second on one core
+        self.pool.map(_cpu_worker, [self._args(0, 1)] * self.cores)  # spawn + imports
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_worker, [self._args(0, 2)])
+        self.t_item = max((time.perf_counter() - t0) / 2, 1e-4)  # one item = T vectors on one core
+
+    def _args(self, a, b):
+        wl = self.wl
+        return (wl["arch"], wl["kind"], self.H[a:b], self.Y[a:b], self.n0[a:b], self.offsets, wl["bits"],
+                wl["t_max"])
+
+    def run(self, seconds):
+        """Run a bounded sample (~`seconds` of wall on all cores).  Returns
+        (Gb/s, items, wall seconds)."""
+        n_items = max(self.cores, int(self.cores * seconds / self.t_item))
+        n_items = min(n_items, self.H.shape[0])
+        # spread the sample over the frames (SNR points) of the workload
+        idx = np.linspace(0, self.H.shape[0] - 1, n_items).astype(int)
+        chunks = np.array_split(idx, self.cores)
+        args = []
+        for c in chunks:
+            if len(c):
+                wl = self.wl
+                args.append((wl["arch"], wl["kind"], self.H[c], self.Y[c], self.n0[c], self.offsets, wl["bits"],
+                             wl["t_max"]))
+        t0 = time.perf_counter()
+        vecs = sum(self.pool.map(_cpu_worker, args))
+        wall = time.perf_counter() - t0
+        bits = vecs * self.wl["U"] * self.wl["bits"]
+        return bits / wall / 1e9, n_items, wall
+
+    def close(self):
+        self.pool.terminate()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------- inputs ----
+def make_inputs(wl, seed=1234, unique_frames=None):
+    from paper_1808_04473_b200.synth import synth_frames
+
+    f = wl["frames"]
+    uf = f if unique_frames is None else min(f, unique_frames)
+    snr = wl["snr"] if len(wl["snr"]) == f else [wl["snr"][0]] * f
+    H, Y, S, n0 = synth_frames(seed, uf, W, T, wl["B"], wl["U"], CONST[wl["bits"]], snr[:uf])
+    if uf < f:  # tile unique frames (cfg5: 25-50 GB per step cannot be generated on the host)
+        reps = math.ceil(f / uf)
+        n0 = np.tile(n0, reps)[:f]
+    return H, Y, n0, uf
+
+
+def reference_arm(args, wl, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    H, Y, n0, uf = make_inputs(wl, unique_frames=min(wl["frames"], 2))
+    n0_items = np.repeat(n0[:uf], W)
+    cpu = CpuBaseline(wl, H, Y, n0_items)
+    for _ in range(args.warmup):
+        cpu.run(0.25)
+    rates, items = [], 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, n, _ = cpu.run(0.5)
+        rates.append(r)
+        items += n
+    wall = time.perf_counter() - t0
+    cpu.close()
+    bits = items * T * wl["U"] * wl["bits"]
+    value = bits / wall / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gb/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+        "data": "synthetic i.i.d. Rayleigh CN(0,1/B), uniform 16/64-QAM, CN(0,N0) noise (seeded)",
+        "config": {"workload": wl_desc(name, wl), "parallelism": f"{cpu.cores} host processes"},
+        "cpu_baseline": {"value": value, "unit": "Gb/s", "cores": cpu.cores, "kind": "port",
+                         "sample": f"{args.steps} steps x ~0.5 s: per-vector oracle port of the reference path "
+                                   f"(oracle/dbp_oracle.py) on {items} (frame,subcarrier) items x {T} symbols, "
+                                   f"CPU {cpu_model()}"},
+        "e2e": {"value": value, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return reference_arm(args, wl, args.config)
+    if world > 1:
+        from paper_1808_04473_b200 import distributed
+
+        return distributed.bench_main(args, wl, args.config, sys.modules[__name__])
+    return single_gpu(args, wl, args.config)
+
+
+def single_gpu(args, wl, name):
+    import torch
+
+    import paper_1808_04473_b200 as dbp
+    from paper_1808_04473_b200 import _lib
+
+    torch.cuda.set_device(0)
+    const = dbp.make_constellation(CONST[wl["bits"]])
+    big = wl["U"] == 64
+    H, Y, n0, uf = make_inputs(wl, unique_frames=2 if big else None)
+    n_items = wl["frames"] * W
+    counts = [wl["B"] // wl["C"]] * wl["C"]
+    lp = {"t_max": wl["t_max"]} if wl["kind"] == "lama" else None
+    det = dbp.Detector(wl["arch"], wl["kind"], n_items, wl["B"], wl["U"], T, counts, const, lama_params=lp)
+    # device-resident inputs; alternate two copies so no step starts from a warm L2
+    Hd = torch.empty((n_items, wl["B"], wl["U"]), dtype=torch.complex64, device="cuda")
+    Yd = torch.empty((n_items, T, wl["B"]), dtype=torch.complex64, device="cuda")
+    Hu, Yu = torch.from_numpy(H).cuda(), torch.from_numpy(Y).cuda()
+    for f in range(wl["frames"]):
+        src = (f % uf) * W
+        Hd[f * W:(f + 1) * W].copy_(Hu[src:src + W])
+        Yd[f * W:(f + 1) * W].copy_(Yu[src:src + W])
+    del Hu, Yu
+    step_bytes = (Hd.numel() + Yd.numel()) * 8
+    copies = [(Hd, Yd)]
+    if step_bytes < 4 * L2_BYTES and torch.cuda.mem_get_info()[0] > 3 * step_bytes:
+        copies.append((Hd.clone(), Yd.clone()))
+    n0_dev = torch.tensor(np.asarray(n0, dtype=np.float32), device="cuda")
+    # parity gate on this very input before timing (first subcarriers of frame 0)
+    out = det.run(Hd, Yd, 0.0, n0_dev, W, check=True)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        h, y = copies[0]
+        det.run(h, y, 0.0, n0_dev, W)
+    torch.cuda.synchronize()
+    det.launches = 0
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for k in range(args.steps):
+            h, y = copies[k % len(copies)]
+            det.run(h, y, 0.0, n0_dev, W)
+        stop.record()
+        torch.cuda.synchronize()
+        # keep sampling clocks for a comparable window if the region was short
+        elapsed_ms = start.elapsed_time(stop)
+        if elapsed_ms < 300:
+            extra = max(1, int(300 / max(elapsed_ms / args.steps, 1e-3)))
+            for k in range(extra):
+                h, y = copies[k % len(copies)]
+                det.run(h, y, 0.0, n0_dev, W)
+            torch.cuda.synchronize()
+    launches = args.steps
+    ms = elapsed_ms / args.steps
+    bits = bits_per_step(wl)
+    value = bits / (ms * 1e-3) / 1e9
+    alg_bytes = algorithmic_bytes(wl, n_items)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)" if "hbm_gbs" in peaks else "fallback"
+    achieved = alg_bytes / (ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
+        traffic = tr.get(name)
+    except Exception:
+        pass
+
+    # ---------------- end to end: host pinned buffers through the public API
+    e2e = None
+    if args.e2e_steps > 0:
+        Hh = torch.empty(Hd.shape, dtype=torch.complex64, pin_memory=True)
+        Yh = torch.empty(Yd.shape, dtype=torch.complex64, pin_memory=True)
+        Hh.copy_(Hd)
+        Yh.copy_(Yd)
+        outs = det.alloc_host_outputs()
+        nchunk = max(8, wl["frames"])
+        bufs = det.device_staging(chunks=nchunk)
+        n0_items_dev = torch.repeat_interleave(n0_dev, W)
+        det.run_host(Hh, Yh, outs, 0.0, n0_items_dev, 1, chunks=nchunk, bufs=bufs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        bi = bo = 0
+        for _ in range(args.e2e_steps):
+            bi, bo = det.run_host(Hh, Yh, outs, 0.0, n0_items_dev, 1, chunks=nchunk, bufs=bufs)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        e2e = {"value": bits / (ems * 1e-3) / 1e9, "unit": "Gb/s", "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo), "ms_per_step": ems,
+               "path": "Detector.run_host: pinned host H,Y -> chunked H2D / fused kernel / D2H of xhat, sigma2, "
+                       "decisions, status (3 streams)"}
+        # sanity: results equal the device-resident run
+        ref = out.decisions.cpu()
+        assert torch.equal(outs["dec"], ref)
+
+    # ---------------- CPU baseline (reference algorithm, host cores)
+    cpu = None
+    if not args.no_cpu:
+        n0_items = np.repeat(n0[:uf], W)
+        cb = CpuBaseline(wl, H, Y, n0_items)
+        rate, n_s, wall = cb.run(args.cpu_seconds)
+        cb.close()
+        cpu = {"value": rate, "unit": "Gb/s", "cores": cb.cores, "kind": "port",
+               "sample": f"{n_s} (frame,subcarrier) items x {T} symbols of this workload through the per-vector "
+                         f"oracle port of the reference path, {wall:.1f} s wall on {cb.cores} processes "
+                         f"({cpu_model()})"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gb/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64 (fp32 arithmetic)",
+        "data": "synthetic: i.i.d. Rayleigh CN(0,1/B) channels constant over T, uniform QAM symbols, "
+                "CN(0,N0) noise, seeded (paper's LTE/WINNER-II data not available)",
+        "config": {"workload": wl_desc(name, wl), "B": wl["B"], "C": wl["C"], "U": wl["U"], "T": T, "W": W,
+                   "frames_per_step": wl["frames"], "snr_db": wl["snr"], "items_per_step": n_items,
+                   "l2": f"inputs {step_bytes / 2**20:.0f} MiB/step vs 126 MiB L2; {len(copies)} input "
+                         f"copies alternated",
+                   "parallelism": "1 GPU, all clusters on chip"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes, "kernel": "dbp::stream_kernel (1 launch/step)"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * dbp_b200.h -- C ABI of libdbp_b200.so, the sm_100a (B200) implementation of
+ * the decentralized feedforward equalization path of arXiv 1808.04473.
+ *
+ * Boundary: the reference (`dbp` Python package, /root/reference/pkg) has no
+ * FFI; its only plugin seam is `dbp.kernels` (kernels.py:13-19,41-50) and its
+ * operator API is the public functions of dbp.equalize / dbp.fusion.  Each
+ * entry point below replaces one of those functions (cited per entry) and is
+ * bound from Python with ctypes by paper_1808_04473_b200/_lib.py.
+ *
+ * Conventions
+ *  - Every data pointer is a DEVICE pointer (cudaMalloc / torch tensor
+ *    data_ptr()).  Complex numbers are interleaved float pairs (complex64).
+ *    Small parameter arrays marked "host" are read synchronously.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *    asynchronous on it.  Calls are reentrant.
+ *  - Return value: DBP_OK, or a negative DBP_E_* code with a message from
+ *    dbp_last_error() (thread-local).
+ *  - Numerical faults are reported per item in `status` (int32, one per
+ *    item), the batched form of the reference's exceptions:
+ *       DBP_ST_SINGULAR   -> SingularGramError   (Cholesky pivot <= 0 /
+ *                            relative fp32 tolerance; MRC diag <= 0; L-MMSE
+ *                            signal gain <= 0)
+ *       DBP_ST_NEGVAR     -> NegativeVarianceError
+ *       DBP_ST_DIVERGED   -> DivergenceError, iteration in `iters`
+ *       DBP_ST_BADVAR     -> ConfigError (fusion weights need sigma2 > 0)
+ *
+ * Layouts (row-major):
+ *   H      [n][B][u_stride]   channel per item (item = (frame, subcarrier)),
+ *                             u_stride even, columns >= u ignored
+ *   Y      [n][T][B]          T receive vectors per item (channel constant
+ *                             over T)
+ *   stats  [n][ncl][u*u + T*u]  Gram G (u x u, full Hermitian) then the
+ *                             matched filter ymrc [T][u]
+ *   xhat   [n][T][u]          estimates;  dec [n][T][u] uint8 symbol index
+ *   sigma2 [n][u] (MRC/ZF/L-MMSE) or [n][T] (LAMA: tau broadcast over u)
+ *   nu     [n][C][u] (linear FD) or [n][C][T] (LAMA FD)
+ *
+ * Limits: u <= 64, T <= 16, C <= 16, cluster row counts and B even, at most
+ * 64 row chunks of 32 per item (B <= 2048).
+ */
+#ifndef DBP_B200_H
+#define DBP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBP_ABI_VERSION 1
+
+#define DBP_OK 0
+#define DBP_E_ARG (-1)
+#define DBP_E_CUDA (-2)
+#define DBP_E_UNSUPPORTED (-3)
+
+#define DBP_ST_OK 0
+#define DBP_ST_SINGULAR 1
+#define DBP_ST_NEGVAR 2
+#define DBP_ST_DIVERGED 3
+#define DBP_ST_BADVAR 4
+
+/* equalizer kinds: equalize.py:27-31 (Equalizer enum) */
+#define DBP_MRC 0
+#define DBP_ZF 1
+#define DBP_LMMSE 2
+#define DBP_LAMA 3
+
+/* architectures: model.py:20-27 (Architecture enum) plus the multi-GPU
+ * FD partial-sum mode */
+#define DBP_ARCH_PD 1
+#define DBP_ARCH_FD 2
+#define DBP_ARCH_FD_PARTIAL 3
+
+int dbp_abi_version(void);
+const char* dbp_last_error(void);
+int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_bytes);
+
+/* Per-cluster Gram + matched filter.  Replaces local_preprocess
+ * (equalize.py:85-93); with sum_clusters=1 also fuse_partials
+ * (equalize.py:96-107) / centralized_stats (:110-112).
+ * offsets: host int32[C+1] row offsets (even).  stats: [n][sum?1:C][...]. */
+int dbp_gram_mrc(const void* H, const void* Y, int64_t n_items, int B, int u,
+                 int u_stride, int T, int C, const int32_t* offsets,
+                 int sum_clusters, void* stats, void* stream);
+
+/* Central equalization from fused statistics.  Replaces linear_equalize
+ * (equalize.py:130-176) + unbiased_output (:179-195) for kind MRC/ZF/LMMSE,
+ * and lama_equalize (:208-259) for kind LAMA (beta, t_max, damping; the
+ * statistics and N0 are multiplied by lama_scale, as cluster_equalize does
+ * with 1/w_c, fusion.py:66-68).  Noise: item i uses n0_dev[i / n0_group]
+ * when n0_dev != NULL, else n0.  Constellation: square-QAM PAM levels
+ * (host float[L], ascending; L=0 for a generic set) and the symbol set
+ * (host float[2*M]).  unbias: write z/c and the unbiased sigma2 (L-MMSE);
+ * gain (nullable) receives c.  dec (nullable): nearest-symbol indices.
+ * tr_* (nullable, LAMA): per-iteration z/s/v [n][t_max][T][u] and
+ * phi [n][t_max][T]. */
+int dbp_equalize_stats(const void* stats, int64_t n_items, int u, int T,
+                       int kind, float n0, const float* n0_dev,
+                       int64_t n0_group, float es, int unbias, float beta,
+                       float lama_scale, int t_max, float damping,
+                       const float* levels, int L, const float* symbols, int M,
+                       void* xhat, float* sigma2, float* gain, uint8_t* dec,
+                       int32_t* status, int32_t* iters, void* tr_z, void* tr_s,
+                       void* tr_v, float* tr_phi, void* stream);
+
+/* Fused single-pass pipeline from (H, Y) to estimates and decisions; the
+ * Gram, matched filter and all per-cluster intermediates stay on chip.
+ *  arch PD: montecarlo.py:131-145 -- sum of all clusters' statistics, then
+ *           the central equalizer (LAMA with beta, lama_scale as above).
+ *  arch FD: fd_equalize (fusion.py:127-154) -- per cluster equalization
+ *           (LAMA on the rescaled system with beta_c = u/B_c, w_c =
+ *           B_c/B_total), unbiasing, inverse-variance (MRC: Gram-diagonal)
+ *           weights, fusion; nu receives the weights.
+ *  arch FD_PARTIAL: as FD but writes the un-normalised fusion sums
+ *           fd_acc [n][2*T*u + 2*wdim] = {sum_c w z, sum_c w, sum_c 1/s2}
+ *           and the raw weights fd_wraw [n][C][wdim] (wdim = u, or T for
+ *           LAMA) for a cross-GPU sum (dbp_fd_finalize / dbp_fd_weights).
+ *  real_counts (host int32[C], nullable): true antenna counts per cluster
+ *  when the rows were zero-padded to even counts; B_total = sum of them. */
+int dbp_equalize(int arch, int kind, const void* H, const void* Y,
+                 int64_t n_items, int B, int u, int u_stride, int T, int C,
+                 const int32_t* offsets, const int32_t* real_counts,
+                 int B_total, float n0, const float* n0_dev, int64_t n0_group,
+                 float es, int unbias, float beta, float lama_scale, int t_max,
+                 float damping, const float* levels, int L,
+                 const float* symbols, int M, void* xhat, float* sigma2,
+                 float* gain, float* nu, uint8_t* dec, int32_t* status,
+                 int32_t* iters, float* fd_acc, float* fd_wraw, void* stream);
+
+/* Finish an FD fusion from summed partials (fuse_estimates,
+ * fusion.py:108-124): xhat = sum w z / sum w, sigma2 = 1 / sum 1/s2. */
+int dbp_fd_finalize(const float* fd_acc, int64_t n_items, int u, int T,
+                    int wdim, const float* levels, int L, const float* symbols,
+                    int M, void* xhat, float* sigma2, uint8_t* dec,
+                    void* stream);
+
+/* nu[n][c][k] = wraw[n][c][k] / den[n][k]  (optimal_fusion_weights,
+ * fusion.py:96-105, with the denominator summed over all GPUs). */
+int dbp_fd_weights(const float* wraw, const float* den, int64_t n_items,
+                   int C, int wdim, float* nu, void* stream);
+
+/* Discrete-posterior mean/variance (kernels.posterior_mean_var,
+ * kernels.py:41-50 -> _kernels.pyx:19-71) for n complex entries. */
+int dbp_posterior(const void* z, int64_t n, float tau, const float* symbols,
+                  int M, void* f_out, float* g_out, void* stream);
+
+/* Nearest-symbol decision, ties to the lowest index (hard_detect,
+ * equalize.py:262-268). */
+int dbp_hard_detect(const void* z, int64_t n, const float* symbols, int M,
+                    int32_t* idx_out, void* stream);
+
+/* fuse_partials (equalize.py:96-107): out[e] = sum_p parts[p*count + e]
+ * over `count` complex entries (P stacked statistics records). */
+int dbp_stats_sum(const void* parts, int P, int64_t count, void* out, void* stream);
+
+/* unbiased_output (equalize.py:179-195) for z [n][T][u], s2/gain [n][u]:
+ * z/c and (s2 - (1-c)^2 Es)/c^2 (clamped at 0); status per item. */
+int dbp_unbias(const void* z, const float* s2, const float* gain, int64_t n, int T, int u, float es, void* z_out,
+               float* s2_out, int32_t* status, void* stream);
+
+/* optimal_fusion_weights (fusion.py:96-105) for s2 [n][C][u] -> nu [n][C][u];
+ * status DBP_ST_BADVAR where some s2 <= 0. */
+int dbp_fusion_weights(const float* s2, int64_t n, int C, int u, float* nu, int32_t* status, void* stream);
+
+/* fuse_estimates (fusion.py:108-124) over z, s2, nu [C][count]:
+ * z_out = sum_c nu z, s2_out = 1 / sum_c 1/max(s2, 1e-15). */
+int dbp_fuse_estimates(const void* z, const float* s2, const float* nu, int C, int64_t count, void* z_out,
+                       float* s2_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBP_B200_H */

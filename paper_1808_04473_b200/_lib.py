@@ -1,0 +1,114 @@
+"""ctypes binding of libdbp_b200.so (include/dbp_b200.h).
+
+The library is loaded lazily on first use.  There is no CPU fallback: a
+missing library, a machine without a CUDA device or a failed launch raise
+:class:`BackendError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import BackendError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdbp_b200.so")
+ABI_VERSION = 1
+
+# status codes (include/dbp_b200.h)
+ST_OK, ST_SINGULAR, ST_NEGVAR, ST_DIVERGED, ST_BADVAR = 0, 1, 2, 3, 4
+KIND = {"mrc": 0, "zf": 1, "lmmse": 2, "lama": 3}
+ARCH_PD, ARCH_FD, ARCH_FD_PARTIAL = 1, 2, 3
+
+_vp, _fp, _i32p, _u8p = C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p
+_i64, _i, _f = C.c_int64, C.c_int, C.c_float
+
+# name -> argtypes (pointers to host parameter arrays are passed as c_void_p)
+SIGNATURES = {
+    "dbp_abi_version": [],
+    "dbp_last_error": [],
+    "dbp_device_query": [_vp, _vp, _vp, _vp],
+    "dbp_gram_mrc": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp],
+    "dbp_equalize_stats": [_vp, _i64, _i, _i, _i, _f, _vp, _i64, _f, _i, _f, _f, _i, _f,
+                           _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dbp_equalize": [_i, _i, _vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _vp, _i, _f, _vp, _i64,
+                     _f, _i, _f, _f, _i, _f, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                     _vp, _vp, _vp],
+    "dbp_fd_finalize": [_vp, _i64, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp],
+    "dbp_fd_weights": [_vp, _vp, _i64, _i, _i, _vp, _vp],
+    "dbp_posterior": [_vp, _i64, _f, _vp, _i, _vp, _vp, _vp],
+    "dbp_hard_detect": [_vp, _i64, _vp, _i, _vp, _vp],
+    "dbp_stats_sum": [_vp, _i, _i64, _vp, _vp],
+    "dbp_unbias": [_vp, _vp, _vp, _i64, _i, _i, _f, _vp, _vp, _vp, _vp],
+    "dbp_fusion_weights": [_vp, _i64, _i, _i, _vp, _vp, _vp],
+    "dbp_fuse_estimates": [_vp, _vp, _vp, _i, _i64, _vp, _vp, _vp],
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load the shared library and declare every exported signature (no GPU
+    needed for this step)."""
+    if not os.path.exists(path):
+        raise BackendError(
+            f"{path} not found: build it with `make` (or __graft_entry__.build()); "
+            "there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_char_p if name == "dbp_last_error" else C.c_int
+    if lib.dbp_abi_version() != ABI_VERSION:
+        raise BackendError("libdbp_b200.so ABI version mismatch; rebuild")
+    return lib
+
+
+def lib():
+    """The loaded library, after checking that a CUDA device is present."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                import torch
+
+                if not torch.cuda.is_available():
+                    raise BackendError("no CUDA device: the sm_100a path has no CPU fallback")
+                _lib = load_library()
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().dbp_last_error().decode(errors="replace")
+        raise BackendError(f"libdbp_b200 error {rc}: {msg}")
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def host_f32(values):
+    """Keep a host float32 parameter array alive and return (array, ptr)."""
+    import numpy as np
+
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.float32).reshape(-1))
+    return arr, (arr.ctypes.data_as(C.c_void_p) if arr.size else None)
+
+
+def host_i32(values):
+    import numpy as np
+
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.int32).reshape(-1))
+    return arr, arr.ctypes.data_as(C.c_void_p)
