@@ -64,8 +64,8 @@ __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a *
 
 // Shared-memory carve-up (byte offsets), identical on host and device.
 struct Layout {
-  int bars, stages, red, G, Z, X, W, Sv, Vv, Fb, gb, num, phi, coef, Ld, s2, gn, dg, den, harm, wbuf,
-      pairs, flags, total;
+  int bars, stages, red, G, Z, X, W, Sv, Vv, Fb, gb, num, phi, coef, s2, gn, dg, den, harm, wbuf,
+      flags, total;
 };
 
 __host__ __device__ inline Layout make_layout(int UP, int NT, int TP, int stage_bytes, int NS,
@@ -88,7 +88,7 @@ __host__ __device__ inline Layout make_layout(int UP, int NT, int TP, int stage_
   L.X = o;
   o += TP * LD * 8;
   L.W = o;
-  o += lama ? 0 : UP * LD * 8;
+  o += lama ? 0 : 4 * UP * 8;
   L.Sv = o;
   o += lama ? TP * LD * 8 : 0;
   L.Vv = o;
@@ -104,8 +104,6 @@ __host__ __device__ inline Layout make_layout(int UP, int NT, int TP, int stage_
   o += TP * 4;
   L.coef = o;
   o += TP * 4;
-  L.Ld = o;
-  o += UP * 4;
   L.s2 = o;
   o += V * 4;
   L.gn = o;
@@ -118,8 +116,6 @@ __host__ __device__ inline Layout make_layout(int UP, int NT, int TP, int stage_
   o += fd ? V * 4 : 0;
   L.wbuf = o;
   o += fd ? C * V * 4 : 0;
-  L.pairs = o;
-  o += align_up(UP * (UP + 1) / 2 * 2, 16);
   L.flags = o;
   o += 16;
   L.total = align_up(o, 128);
@@ -139,11 +135,9 @@ __device__ __forceinline__ Work make_work(char* smem, const Layout& L, int UP) {
   w.gb = reinterpret_cast<float*>(smem + L.gb);
   w.phi = reinterpret_cast<float*>(smem + L.phi);
   w.coef = reinterpret_cast<float*>(smem + L.coef);
-  w.Ld = reinterpret_cast<float*>(smem + L.Ld);
   w.s2 = reinterpret_cast<float*>(smem + L.s2);
   w.gn = reinterpret_cast<float*>(smem + L.gn);
   w.dg = reinterpret_cast<float*>(smem + L.dg);
-  w.pairs = reinterpret_cast<uint16_t*>(smem + L.pairs);
   w.flags = reinterpret_cast<int*>(smem + L.flags);
   w.LD = UP + 1;
   return w;
@@ -222,59 +216,42 @@ __device__ __forceinline__ void accumulate_chunk(float2 (&acc)[4][4], const floa
 }
 
 // Reduce the K groups' tiles into G / Z (shared), then zero the accumulators.
+// Groups g >= 1 park their partial tiles in `red`; the g == 0 owner of each
+// tile adds them and writes the tile (and its Hermitian mirror).
 template <int UP, int NT>
 __device__ __forceinline__ void reduce_tiles(float2 (&acc)[4][4], const TileInfo& ti, float2* red, const Work& w,
                                              int T, int ntiles) {
   const int tid = threadIdx.x;
   const int LD = w.LD;
-  if (ti.S == 1) {
-    if (ti.active) {
+  if (ti.S > 1) {
+    const int tile = tid % ntiles;
+    if (ti.active && ti.g > 0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i = 4 * ti.ib + r;
-          if (ti.isz) {
-            const int t = 4 * ti.jb + c;
-            if (t < T) w.Z[t * LD + i] = acc[r][c];
-          } else {
-            const int j = 4 * ti.jb + c;
-            w.G[i * LD + j] = acc[r][c];
-            if (ti.ib != ti.jb) w.G[j * LD + i] = c_conj(acc[r][c]);
-          }
-        }
-    }
-  } else {
-    if (ti.active) {
-      const int tile = tid % ntiles;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) red[(ti.g * 16 + e) * ntiles + tile] = acc[e >> 2][e & 3];
+      for (int e = 0; e < 16; ++e) red[((ti.g - 1) * 16 + e) * ntiles + tile] = acc[e >> 2][e & 3];
     }
     __syncthreads();
-    for (int f = tid; f < 16 * ntiles; f += NT) {
-      float2 s = red[f];
-      for (int g = 1; g < ti.S; ++g) s = c_add(s, red[g * 16 * ntiles + f]);
-      const int e = f / ntiles, tile = f - e * ntiles;
-      const int r = e >> 2, c = e & 3;
-      // decode tile (same enumeration as decode_tile)
-      constexpr int UB = UP / 4;
-      constexpr int NG = UB * (UB + 1) / 2;
-      if (tile < NG) {
-        int rr = tile, ib = 0;
-        while (rr >= UB - ib) {
-          rr -= UB - ib;
-          ++ib;
-        }
-        const int jb = ib + rr;
-        const int i = 4 * ib + r, j = 4 * jb + c;
-        w.G[i * LD + j] = s;
-        if (ib != jb) w.G[j * LD + i] = c_conj(s);
-      } else {
-        const int z = tile - NG;
-        const int i = 4 * (z % UB) + r, t = 4 * (z / UB) + c;
-        if (t < T) w.Z[t * LD + i] = s;
-      }
+    if (ti.g == 0) {
+      for (int g = 1; g < ti.S; ++g)
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          acc[e >> 2][e & 3] = c_add(acc[e >> 2][e & 3], red[((g - 1) * 16 + e) * ntiles + tile]);
     }
+  }
+  if (ti.active && ti.g == 0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * ti.ib + r;
+        if (ti.isz) {
+          const int t = 4 * ti.jb + c;
+          if (t < T) w.Z[t * LD + i] = acc[r][c];
+        } else {
+          const int j = 4 * ti.jb + c;
+          w.G[i * LD + j] = acc[r][c];
+          if (ti.ib != ti.jb) w.G[j * LD + i] = c_conj(acc[r][c]);
+        }
+      }
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -298,7 +275,7 @@ __device__ __forceinline__ void store_estimates(const Work& w, const EqParams& p
 }
 
 // The unit epilogue for PD / single-cluster calls: equalize, write outputs.
-template <int NT>
+template <int UP, int NT>
 __device__ void pd_epilogue(const Work& w, const EqParams& p, int64_t n, float n0) {
   EpiArgs a;
   a.kind = p.kind;
@@ -328,7 +305,7 @@ __device__ void pd_epilogue(const Work& w, const EqParams& p, int64_t n, float n
     store_estimates<NT>(w, p, n, false);
     for (int t = tid; t < p.T; t += NT) p.sigma2[(size_t)n * p.T + t] = w.s2[t];
   } else {
-    linear_unit<NT>(w, a);
+    linear_unit<UP, NT>(w, a);
     store_estimates<NT>(w, p, n, false);
     for (int i = tid; i < p.u; i += NT) {
       p.sigma2[(size_t)n * p.u + i] = w.s2[i];
@@ -385,7 +362,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
   constexpr int NG = UB * (UB + 1) / 2;
   const int ntiles = NG + UB * TB;
   const TileInfo ti = decode_tile<UP>(tid, TB, NT);
-  const int red_f2 = (ti.S > 1) ? ti.S * ntiles * 16 : 0;
+  const int red_f2 = (ti.S > 1) ? (ti.S - 1) * ntiles * 16 : 0;
   const Layout L = make_layout(UP, NT, p.TP, p.stage_f2 * 8, p.NS, p.C, red_f2, lama, fd);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   float2* red = reinterpret_cast<float2*>(smem + L.red);
@@ -395,12 +372,6 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
   float* harm = reinterpret_cast<float*>(smem + L.harm);
   float* wbuf = reinterpret_cast<float*>(smem + L.wbuf);
 
-  // pair table of the lower triangle, row-major: p -> (ii, kk), kk <= ii
-  for (int q = tid; q < UP * (UP + 1) / 2; q += NT) {
-    int ii = 0;
-    while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
-    w.pairs[q] = (uint16_t)((ii << 8) | (q - ii * (ii + 1) / 2));
-  }
   if (tid == 0) {
     for (int s = 0; s < p.NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -416,11 +387,12 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 
   auto issue = [&](int64_t q) {
     if (q >= total) return;
-    const int64_t il = q / p.nchunks;
-    const int j = (int)(q - il * p.nchunks);
-    const int64_t n = blockIdx.x + il * gridDim.x;
+    const int qi = (int)q;
+    const int il = qi / p.nchunks;
+    const int j = qi - il * p.nchunks;
+    const int64_t n = blockIdx.x + (int64_t)il * gridDim.x;
     const ChunkDesc cd = p.chunks[j];
-    const int s = (int)(q % p.NS);
+    const int s = qi % p.NS;
     char* st = smem + L.stages + s * stage_bytes;
     const uint32_t hbytes = (uint32_t)cd.nrows * p.us * 8;
     const uint32_t ybytes = (uint32_t)cd.nrows * 8;
@@ -440,13 +412,22 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
     for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
 
   int cl_first = 1;  // FD: first cluster of the current item
+  int jn = 0, sn = 0;  // chunk-in-item and stage of the next chunk
+  uint32_t phase = 0;
+  int64_t nn = blockIdx.x;
   for (int64_t q = 0; q < total; ++q) {
-    const int64_t il = q / p.nchunks;
-    const int j = (int)(q - il * p.nchunks);
-    const int64_t n = blockIdx.x + il * gridDim.x;
-    const ChunkDesc cd = p.chunks[j];
-    const int s = (int)(q % p.NS);
-    mbar_wait(&bars[s], (uint32_t)((q / p.NS) & 1));
+    const ChunkDesc cd = p.chunks[jn];
+    const int s = sn;
+    const int64_t n = nn;
+    mbar_wait(&bars[s], phase);
+    if (++sn == p.NS) {
+      sn = 0;
+      phase ^= 1u;
+    }
+    if (++jn == p.nchunks) {
+      jn = 0;
+      nn += gridDim.x;
+    }
     const float2* Hs = reinterpret_cast<const float2*>(smem + L.stages + s * stage_bytes);
     const float2* Ys = Hs + p.KC * p.us;
     if (ti.active) accumulate_chunk(acc, Hs, Ys, cd.nrows, p.us, p.KCP, ti);
@@ -472,7 +453,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
       continue;
     }
     if (p.arch == ARCH_PD) {
-      pd_epilogue<NT>(w, p, n, n0);
+      pd_epilogue<UP, NT>(w, p, n, n0);
       __syncthreads();
       if (tid == 0) {
         w.flags[0] = 0;
@@ -498,7 +479,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
       if (lama)
         lama_unit<NT>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr);
       else
-        linear_unit<NT>(w, a);
+        linear_unit<UP, NT>(w, a);
       fd_accumulate<NT>(w, num, den, harm, wbuf, p, c, cl_first != 0);
       __syncthreads();
       cl_first = 0;
@@ -564,11 +545,6 @@ __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqPar
   const bool lama = p.kind == EQ_LAMA;
   const Layout L = make_layout(UP, NT, p.TP, 0, 0, 1, 0, lama, false);
   Work w = make_work(smem, L, UP);
-  for (int q = tid; q < UP * (UP + 1) / 2; q += NT) {
-    int ii = 0;
-    while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
-    w.pairs[q] = (uint16_t)((ii << 8) | (q - ii * (ii + 1) / 2));
-  }
   const int u = p.u, T = p.T;
   const size_t rec = (size_t)u * u + (size_t)T * u;
   for (int64_t n = blockIdx.x; n < p.n_items; n += gridDim.x) {
@@ -580,7 +556,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqPar
     for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
     for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
     __syncthreads();
-    pd_epilogue<NT>(w, p, n, item_n0(p, n));
+    pd_epilogue<UP, NT>(w, p, n, item_n0(p, n));
     __syncthreads();
   }
 }
@@ -761,7 +737,7 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
   const int ntiles = UB * (UB + 1) / 2 + UB * TB;
   const int S = NT / ntiles;
   if (S < 1) return fail(DBP_E_UNSUPPORTED, "too many output tiles for the CTA (u, T too large)");
-  const int red_f2 = S > 1 ? S * ntiles * 16 : 0;
+  const int red_f2 = S > 1 ? (S - 1) * ntiles * 16 : 0;
   const Layout L = make_layout(UP, NT, p.TP, p.stage_f2 * 8, p.NS, p.C, red_f2, lama, fd);
   auto kern = stream_kernel<UP, NT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
