@@ -1,0 +1,54 @@
+"""The multi-GPU code path (distributed.CudaOps: K1 stats -> NCCL
+reduce-scatter -> central solve; FD partial sums -> reduce-scatter ->
+finalize, weight all-reduce) on the one available B200 as a 1-rank NCCL group.
+Every kernel and collective call of the N-GPU path runs; the result must equal
+the fused single-GPU detector."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1808_04473_b200 as dbp
+from parity import normwise_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("arch,kind", [("pd", "lmmse"), ("pd", "zf"), ("pd", "lama"), ("fd", "lmmse"),
+                                       ("fd", "mrc"), ("fd", "lama")])
+def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
+    from paper_1808_04473_b200.distributed import ClusterGroup
+
+    g = golden("cfg4" if kind == "lama" else "cfg2")
+    const = dbp.make_constellation("qam16")
+    b, c, u = int(g["B"]), int(g["C"]), int(g["U"])
+    H = torch.from_numpy(g["H"]).cuda()
+    Y = torch.from_numpy(g["Y"]).cuda()
+    n0 = torch.tensor(g["n0"], dtype=torch.float32, device="cuda")
+    lp = {"t_max": 10} if kind == "lama" else None
+    grp = ClusterGroup(arch, kind, [b // c] * c, u, Y.shape[1], const, lama_params=lp)
+    res = grp.run(H, Y, n0)
+    ref = dbp.detect(arch, kind, g["H"], g["Y"], g["n0"], [b // c] * c, const, lama_params=lp)
+    assert res.items == (0, H.shape[0])
+    assert normwise_rel(res.xhat.cpu().numpy(), ref.xhat) < 2e-6
+    assert np.mean(res.decisions.cpu().numpy() != ref.decisions) < 1e-3
+    if arch == "fd":
+        assert np.max(np.abs(res.nu.cpu().numpy() - ref.nu)) < 2e-6
