@@ -1,28 +1,76 @@
-// Per-unit (item or cluster) epilogues that run on the on-chip Gram G and
-// matched filter Z: MRC / ZF / L-MMSE (Cholesky + triangular solves), the
-// Gram-domain LAMA recursion, FD fusion accumulation.  All CTA-cooperative on
-// shared memory; the caller provides __syncthreads() boundaries between
-// units.
+// Per-unit epilogues that run on the on-chip Gram G and matched filter Z of
+// one unit (a whole item for PD, one cluster for FD): MRC / ZF / L-MMSE
+// (Gauss-Jordan inverse), the Gram-domain LAMA recursion, FD fusion, the
+// statistics writer and the output stores.  Every function runs on a thread
+// Team (the whole CTA, or the epilogue warps of a warp-specialized kernel)
+// and only synchronises through Team::sync().
 #pragma once
 #include "dbp_device.cuh"
 
 namespace dbp {
 
+struct EqParams {
+  const float2* H;
+  const float2* Y;
+  const float2* stats_in;
+  int64_t n_items;
+  int B, u, us, T, TP;
+  int KC, KCP, NS;
+  int stage_f2;  // float2 elements per raw stage
+  int nchunks;
+  int C;
+  int arch;
+  int kind;
+  int unbias;
+  int sum_clusters;
+  float n0;
+  const float* n0_dev;
+  int64_t n0_group;
+  float es;
+  float beta, lama_scale, damping;
+  int t_max;
+  float cl_scale[MAX_C];
+  float cl_beta[MAX_C];
+  ChunkDesc chunks[MAX_CHUNKS];
+  ConstParams cp;
+  // outputs
+  float2* xhat;
+  float* sigma2;
+  float* gain;
+  float* nu;
+  uint8_t* dec;
+  int32_t* status;
+  int32_t* iters;
+  float2* stats_out;
+  float* fd_acc;
+  float* fd_wraw;
+  float2 *tr_z, *tr_s, *tr_v;
+  float* tr_phi;
+};
+
+__device__ __forceinline__ float item_n0(const EqParams& p, int64_t n) {
+  return p.n0_dev ? p.n0_dev[n / p.n0_group] : p.n0;
+}
+
 // Shared-memory views of one unit's working set (padded leading dims).
 struct Work {
-  float2* G;     // [UP][LD]  Gram; after Cholesky: upper = L^H, Ld = diag(L)
+  float2* G;     // [UP][LD]  Gram -> inverse after Gauss-Jordan
   float2* Z;     // [TP][LD]  matched filter y_mrc per OFDM symbol
   float2* X;     // [TP][LD]  per-symbol solution / LAMA z
-  float2* W;     // scratch: Gauss-Jordan pivot row/column buffers [4][UP]
+  float2* W;     // [4][UP]   Gauss-Jordan pivot row/column buffers
   float2* Sv;    // [TP][LD]  LAMA mean s
   float2* Vv;    // [TP][LD]  LAMA Onsager term v
   float2* Fb;    // [TP][LD]  LAMA posterior mean
   float* gb;     // [TP][LD]  LAMA posterior variance
   float* phi;    // [TP]
   float* coef;   // [TP]
-  float* s2;     // [UP] linear sigma2 (or [TP] for LAMA)
+  float* s2;     // [max(UP,TP)] linear sigma2 (or per-symbol LAMA tau)
   float* gn;     // [UP] MRC gain d / L-MMSE signal gain c
   float* dg;     // [UP] original diagonal (pivot tolerance)
+  float2* num;   // FD [TP][LD] sum_c w z
+  float* den;    // FD [max(UP,TP)] sum_c w
+  float* harm;   // FD [max(UP,TP)] sum_c 1/sigma2
+  float* wbuf;   // FD [C][max(UP,TP)] raw weights
   int* flags;    // [0] status, [1] divergence iteration
   int LD;
 };
@@ -48,13 +96,14 @@ __device__ __forceinline__ void set_status(int* flags, int st) { atomicCAS(flags
 // The inverse is an in-place Gauss-Jordan sweep without pivoting (stable for
 // Hermitian positive definite matrices, like Cholesky): matrix elements stay
 // in registers, each step publishes the old pivot row/column through shared
-// memory (double-buffered, one __syncthreads per step).  A pivot below
+// memory (double-buffered, one team barrier per step).  A pivot below
 // 8*u*eps of its original diagonal is SingularGramError: the fp32 counterpart
 // of zpotrf's "not positive definite" (a rank-deficient fp32 Gram leaves
 // rounding noise ~eps*G_jj instead of an exact zero).
-template <int UP, int NT>
-__device__ void linear_unit(const Work& w, const EpiArgs& a) {
-  const int tid = threadIdx.x;
+template <int UP, class TM>
+__device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
+  constexpr int NT = TM::N;
+  const int tid = tm.t;
   const int u = a.u, T = a.T, LD = w.LD;
   if (a.kind == EQ_MRC) {
     for (int i = tid; i < u; i += NT) {
@@ -67,12 +116,12 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a) {
       w.s2[i] = a.n0 * rd + a.es * off * rd * rd;
       w.gn[i] = d;
     }
-    __syncthreads();
+    tm.sync();
     for (int e = tid; e < T * u; e += NT) {
       const int t = e / u, i = e - t * u;
       w.X[t * LD + i] = c_scale(w.Z[t * LD + i], 1.f / w.gn[i]);
     }
-    __syncthreads();
+    tm.sync();
     return;
   }
   const float rho = (a.kind == EQ_LMMSE) ? a.n0 / a.es : 0.f;
@@ -108,7 +157,7 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a) {
         if (j == k) ck[i] = m[r];
       }
     }
-    __syncthreads();
+    tm.sync();
     float p = rk[k].x;
     if (!(p > tolf * w.dg[k])) {
       if (tid == 0) set_status(w.flags, ST_SINGULAR);
@@ -136,7 +185,7 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a) {
     const int i = e / UP, j = e % UP;
     if (e < UP * UP && i < u && j < u) w.G[i * LD + j] = m[r];
   }
-  __syncthreads();
+  tm.sync();
   // z = A y_mrc per OFDM symbol (+ unbiasing), variances from diag(A)
   const bool unb = (a.kind == EQ_LMMSE) && a.unbias;
   for (int e = tid; e < T * u; e += NT) {
@@ -160,17 +209,18 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a) {
       w.s2[i] = a.unbias ? a.n0 * aii / c : a.n0 * aii;
     }
   }
-  __syncthreads();
+  tm.sync();
 }
 
 // ---- LAMA (equalize.py:208-259) on (G, Z) scaled by lama_scale ----------
 // Per OFDM symbol t an independent recursion; state in shared memory.
 // Output: X = z^{t_max}, s2[t] = tau^{t_max}.  The last iteration skips the
 // denoiser (its F, G only feed discarded updates).
-template <int NT>
-__device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z,
-                          float2* tr_s, float2* tr_v, float* tr_phi) {
-  const int tid = threadIdx.x;
+template <class TM>
+__device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z, float2* tr_s,
+                          float2* tr_v, float* tr_phi, const TM& tm) {
+  constexpr int NT = TM::N;
+  const int tid = tm.t;
   const int u = a.u, T = a.T, LD = w.LD;
   const float sc = a.lama_scale;
   const float n0 = a.n0 * sc;
@@ -186,7 +236,7 @@ __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp
     w.Vv[t * LD + i] = make_float2(0.f, 0.f);
   }
   for (int t = tid; t < T; t += NT) w.phi[t] = cp.es;
-  __syncthreads();
+  tm.sync();
   for (int it = 1; it <= a.t_max; ++it) {
     const bool last = (it == a.t_max);
     for (int e = tid; e < T * u; e += NT) {
@@ -215,7 +265,7 @@ __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp
         w.gb[t * LD + i] = g;
       }
     }
-    __syncthreads();
+    tm.sync();
     if (last) break;
     for (int t = tid; t < T; t += NT) {
       float sum = 0.f;
@@ -225,17 +275,165 @@ __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp
       w.coef[t] = beta * phin / tau;
       w.phi[t] = phin;
     }
-    __syncthreads();
+    tm.sync();
     for (int e = tid; e < T * u; e += NT) {
       const int t = e / u, i = e - t * u;
       const float2 s = w.Sv[t * LD + i];
       w.Vv[t * LD + i] = c_scale(c_sub(w.X[t * LD + i], s), w.coef[t]);
       w.Sv[t * LD + i] = c_add(c_scale(w.Fb[t * LD + i], a.damping), c_scale(s, 1.f - a.damping));
     }
-    __syncthreads();
+    tm.sync();
   }
   for (int t = tid; t < T; t += NT) w.s2[t] = n0 + beta * w.phi[t];
-  __syncthreads();
+  tm.sync();
+}
+
+template <class TM>
+__device__ __forceinline__ void reset_flags(const Work& w, const TM& tm) {
+  if (tm.t == 0) {
+    w.flags[0] = 0;
+    w.flags[1] = 0x7fffffff;
+  }
+}
+
+template <class TM>
+__device__ __forceinline__ void write_status(const Work& w, const EqParams& p, int64_t n, const TM& tm) {
+  if (tm.t == 0) {
+    int st = w.flags[0];
+    if (w.flags[1] < 0x7fffffff) st = st ? st : ST_DIVERGED;
+    p.status[n] = st;
+    if (p.iters) p.iters[n] = (w.flags[1] < 0x7fffffff) ? w.flags[1] : 0;
+  }
+}
+
+// The unit epilogue after G and Z of one unit are in shared memory (and the
+// team is synchronised).  PD: equalize + outputs; FD: equalize one cluster +
+// fold into the fusion sums, finalize on the item's last cluster; STATS:
+// write {G, y_mrc}.  Ends with a team barrier.
+template <int UP, class TM>
+__device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int cluster, bool item_end,
+                              int& cl_first, const TM& tm) {
+  constexpr int NT = TM::N;
+  const int tid = tm.t;
+  const int u = p.u, T = p.T, LD = w.LD;
+  if (p.arch == ARCH_STATS) {
+    const int ncl = p.sum_clusters ? 1 : p.C;
+    const int cl = p.sum_clusters ? 0 : cluster;
+    float2* dst = p.stats_out + ((size_t)n * ncl + cl) * (size_t)(u * u + T * u);
+    for (int e = tid; e < u * u; e += NT) dst[e] = w.G[(e / u) * LD + (e % u)];
+    for (int e = tid; e < T * u; e += NT) dst[u * u + e] = w.Z[(e / u) * LD + (e % u)];
+    tm.sync();
+    return;
+  }
+  const float n0 = item_n0(p, n);
+  const bool lama = p.kind == EQ_LAMA;
+  EpiArgs a;
+  a.kind = p.kind;
+  a.u = u;
+  a.T = T;
+  a.n0 = n0;
+  a.es = p.es;
+  a.damping = p.damping;
+  a.t_max = p.t_max;
+  if (p.arch == ARCH_PD) {
+    a.beta = p.beta;
+    a.lama_scale = p.lama_scale;
+    a.unbias = p.unbias != 0;
+    if (lama) {
+      float2 *tz = nullptr, *ts = nullptr, *tv = nullptr;
+      float* tp = nullptr;
+      if (p.tr_z) {
+        const size_t o = (size_t)n * p.t_max * T * u;
+        tz = p.tr_z + o;
+        ts = p.tr_s + o;
+        tv = p.tr_v + o;
+        tp = p.tr_phi + (size_t)n * p.t_max * T;
+      }
+      lama_unit(w, a, p.cp, tz, ts, tv, tp, tm);
+    } else {
+      linear_unit<UP>(w, a, tm);
+    }
+    for (int e = tid; e < T * u; e += NT) {
+      const int t = e / u, i = e - t * u;
+      const float2 x = w.X[t * LD + i];
+      const size_t o = ((size_t)n * T + t) * u + i;
+      p.xhat[o] = x;
+      if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+    }
+    if (lama) {
+      for (int t = tid; t < T; t += NT) p.sigma2[(size_t)n * T + t] = w.s2[t];
+    } else {
+      for (int i = tid; i < u; i += NT) {
+        p.sigma2[(size_t)n * u + i] = w.s2[i];
+        if (p.gain && (p.kind == EQ_LMMSE || p.kind == EQ_MRC)) p.gain[(size_t)n * u + i] = w.gn[i];
+      }
+    }
+    write_status(w, p, n, tm);
+    tm.sync();
+    reset_flags(w, tm);
+    return;  // the next unit's writes to G/Z follow a barrier in the caller
+  }
+  // ---- FD: equalize this cluster (fusion.py:141-148), fold into the sums ----
+  a.beta = p.cl_beta[cluster];
+  a.lama_scale = p.cl_scale[cluster];
+  a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
+  if (lama)
+    lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
+  else
+    linear_unit<UP>(w, a, tm);
+  // weights: MRC -> Gram diagonal (fusion.py:149-151), otherwise
+  // 1/max(sigma2, 1e-15) (fusion.py:96-105); sigma2 <= 0 is a ConfigError
+  const int wdim = lama ? T : u;
+  const bool first = cl_first != 0;
+  for (int e = tid; e < wdim; e += NT) {
+    const float s2 = w.s2[e];
+    if (p.kind != EQ_MRC && !(s2 > 0.f)) set_status(w.flags, ST_BADVAR);
+    const float inv = 1.f / fmaxf(s2, VAR_FLOOR);
+    const float wt = (p.kind == EQ_MRC) ? w.gn[e] : inv;
+    w.wbuf[cluster * wdim + e] = wt;
+    w.den[e] = first ? wt : w.den[e] + wt;
+    w.harm[e] = first ? inv : w.harm[e] + inv;
+  }
+  tm.sync();
+  for (int e = tid; e < T * u; e += NT) {
+    const int t = e / u, i = e - t * u;
+    const float wt = w.wbuf[cluster * wdim + (lama ? t : i)];
+    const float2 x = c_scale(w.X[t * LD + i], wt);
+    w.num[t * LD + i] = first ? x : c_add(w.num[t * LD + i], x);
+  }
+  tm.sync();
+  cl_first = 0;
+  if (!item_end) return;
+  if (p.arch == ARCH_FD) {
+    for (int e = tid; e < T * u; e += NT) {
+      const int t = e / u, i = e - t * u;
+      const float2 x = c_scale(w.num[t * LD + i], 1.f / w.den[lama ? t : i]);
+      const size_t o = ((size_t)n * T + t) * u + i;
+      p.xhat[o] = x;
+      if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+    }
+    for (int e = tid; e < wdim; e += NT) p.sigma2[(size_t)n * wdim + e] = 1.f / w.harm[e];
+    if (p.nu)
+      for (int e = tid; e < p.C * wdim; e += NT) p.nu[(size_t)n * p.C * wdim + e] = w.wbuf[e] / w.den[e % wdim];
+  } else {  // FD_PARTIAL: raw sums for a cross-GPU reduction
+    const int rec = 2 * T * u + 2 * wdim;
+    float* dst = p.fd_acc + (size_t)n * rec;
+    for (int e = tid; e < T * u; e += NT) {
+      const int t = e / u, i = e - t * u;
+      const float2 v = w.num[t * LD + i];
+      dst[2 * e] = v.x;
+      dst[2 * e + 1] = v.y;
+    }
+    for (int e = tid; e < wdim; e += NT) {
+      dst[2 * T * u + e] = w.den[e];
+      dst[2 * T * u + wdim + e] = w.harm[e];
+    }
+    for (int e = tid; e < p.C * wdim; e += NT) p.fd_wraw[(size_t)n * p.C * wdim + e] = w.wbuf[e];
+  }
+  write_status(w, p, n, tm);
+  tm.sync();
+  reset_flags(w, tm);
+  cl_first = 1;
 }
 
 }  // namespace dbp

@@ -1,0 +1,302 @@
+// Warp-specialized tensor-core streaming kernel (U <= 32).
+//
+// The Gram and the matched filter of one unit are one real GEMM:
+//     P = Xr^T Hr,   Xr = [Re H | Im H | Re Y^T | Im Y^T]  (K = antennas),
+//                    Hr = [Re H | Im H]      (columns interleaved re/im)
+// M = 2(U+T) <= 128 rows, N = 2U, K = B.  G and y_mrc follow from P:
+//     G[u][v]   = P[(u,re)][(v,re)] + P[(u,im)][(v,im)]
+//               + i (P[(u,re)][(v,im)] - P[(u,im)][(v,re)])
+//     y_t[v]    = P[(t,re)][(v,re)] + P[(t,im)][(v,im)]
+//               + i (P[(t,im)][(v,re)] - P[(t,re)][(v,im)])
+// It runs on tcgen05 (kind::tf32, M=128, accumulator in TMEM) with a 3xTF32
+// split (x = hi + lo, P = hi.hi + hi.lo + lo.hi) so the result keeps fp32
+// accuracy (plain TF32 would miss the 1e-4 tolerance: SURVEY.md 8(c)).
+//
+// Roles (8 warps):
+//   warp 0      TMA producer: bulk copies of each chunk (<= 32 antenna rows
+//               of one cluster) of H and Y into a ring of raw stages
+//   warp 1      MMA issuer (one thread): 3 x ceil(rows/8) tcgen05.mma per
+//               chunk into one of two TMEM accumulator slots
+//   warps 2-3   converters: raw stage -> hi/lo operand tiles in the canonical
+//               K-major core-matrix layout (8 rows x 16 B per core matrix)
+//   warps 4-7   epilogue: tcgen05.ld the accumulator (warp w owns TMEM lanes
+//               32(w%4)..+31), assemble G / y_mrc, then the unit epilogue
+//               (solve, FD fusion, stores) on a named barrier
+// Everything is pipelined through mbarriers, so the loads and MMAs of the
+// next units overlap the epilogue of the current one.
+#pragma once
+#include "dbp_simt.cuh"
+
+namespace dbp {
+
+constexpr int TC_THREADS = 256;
+constexpr int TC_CONV = 64;   // converter threads (warps 2-3)
+constexpr int TC_EPI = 128;   // epilogue threads (warps 4-7)
+constexpr int TC_OPB_K = 32;  // antenna rows per operand tile (= KC)
+
+struct TcLayout {
+  int bars, tmem_slot, raw, ops, opb, slack;
+  WorkLayout w;
+  int total;
+};
+
+__host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int stage_bytes, int NS, int C, bool lama,
+                                                   bool fd) {
+  TcLayout L;
+  const int MB = (2 * UP + 2 * T + 7) / 8;  // 8-row core-matrix blocks used
+  int o = 0;
+  L.bars = o;
+  o += (2 * NS + 8) * 8;
+  L.tmem_slot = o;
+  o += 16;
+  o = align_up(o, 128);
+  L.raw = o;
+  o += NS * stage_bytes;
+  o = align_up(o, 1024);
+  L.ops = o;
+  L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
+  o += 4 * L.opb;     // [hi0][lo0][hi1][lo1]
+  // the M=128 MMA reads 16 blocks from each tile base; rows past MB*8 are
+  // never written and only produce ignored accumulator rows
+  L.slack = (16 - MB) * 1024;
+  o += L.slack;
+  L.w = make_work_layout(o, UP, TP, C, lama, fd);
+  L.total = L.w.total;
+  return L;
+}
+
+template <int UP>
+__global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  constexpr int N = 2 * UP;
+  constexpr uint32_t TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool lama = p.kind == EQ_LAMA;
+  const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
+  const int NS = p.NS;
+  const int MU = 2 * UP + 2 * p.T;
+  const int MB = (MU + 7) / 8;
+  const int stage_bytes = p.stage_f2 * 8;
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, stage_bytes, NS, p.C, lama, fd);
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* raw_empty = raw_full + NS;
+  uint64_t* op_full = raw_empty + NS;
+  uint64_t* op_empty = op_full + 2;
+  uint64_t* acc_full = op_empty + 2;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+  const Work w = make_work(smem, L.w, UP);
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_empty[s], TC_CONV);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&op_full[b], TC_CONV);
+      mbar_init(&op_empty[b], 1);
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], TC_EPI);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (tid == TC_THREADS - TC_EPI) {
+    w.flags[0] = 0;
+    w.flags[1] = 0x7fffffff;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t my_items = (p.n_items > blockIdx.x) ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total = (int)(my_items * p.nchunks);
+  const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer ----
+    if (lane == 0) {
+      const uint64_t policy = l2_evict_first_policy();
+      int j = 0, s = 0;
+      uint32_t ph = 0;
+      int64_t n = blockIdx.x;
+      for (int q = 0; q < total; ++q) {
+        if (q >= NS) mbar_wait(&raw_empty[s], ph ^ 1u);
+        const ChunkDesc cd = p.chunks[j];
+        char* st = smem + L.raw + s * stage_bytes;
+        const uint32_t hbytes = (uint32_t)cd.nrows * p.us * 8;
+        const uint32_t ybytes = (uint32_t)cd.nrows * 8;
+        mbar_arrive_expect_tx(&raw_full[s], hbytes + ybytes * p.T);
+        bulk_g2s(st, p.H + ((size_t)n * p.B + cd.row0) * p.us, hbytes, &raw_full[s], policy);
+        float2* ys = reinterpret_cast<float2*>(st) + p.KC * p.us;
+        const float2* ysrc = p.Y + (size_t)n * p.T * p.B + cd.row0;
+        for (int t = 0; t < p.T; ++t)
+          bulk_g2s(ys + t * p.KCP, ysrc + (size_t)t * p.B, ybytes, &raw_full[s], policy);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+        if (++j == p.nchunks) {
+          j = 0;
+          n += gridDim.x;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer ----
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_tf32(128, N);
+      const uint32_t ops = smem_u32(smem + L.ops);
+      int j = 0, unit = 0;
+      bool first = true;
+      for (int q = 0; q < total; ++q) {
+        const int b = q & 1;
+        mbar_wait(&op_full[b], (uint32_t)((q >> 1) & 1));
+        const ChunkDesc cd = p.chunks[j];
+        const int a = unit & 1;
+        if (first && unit >= 2) mbar_wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(a * N);
+        const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
+        const uint32_t lo = hi + (uint32_t)L.opb;
+        const int nk8 = (cd.nrows + 7) >> 3;
+        for (int ks = 0; ks < nk8; ++ks) {
+          const uint64_t ah = umma_desc(hi + ks * 256, 128, 1024);
+          const uint64_t al = umma_desc(lo + ks * 256, 128, 1024);
+          umma_tf32(d, ah, ah, idesc, (first && ks == 0) ? 0u : 1u);
+          umma_tf32(d, ah, al, idesc, 1u);
+          umma_tf32(d, al, ah, idesc, 1u);
+        }
+        umma_commit(&op_empty[b]);
+        const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
+        if (unit_end) {
+          umma_commit(&acc_full[a]);
+          ++unit;
+        }
+        first = unit_end;
+        if (++j == p.nchunks) j = 0;
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // -------------------------------------------------------- converters ----
+    const int ct = tid - 64;
+    const int MBr = MB * 8;
+    const int us2 = 2 * p.us;
+    int j = 0, s = 0;
+    uint32_t ph = 0;
+    for (int q = 0; q < total; ++q) {
+      const int b = q & 1;
+      mbar_wait(&raw_full[s], ph);
+      if (q >= 2) mbar_wait(&op_empty[b], (uint32_t)(((q >> 1) - 1) & 1));
+      const ChunkDesc cd = p.chunks[j];
+      const float* Hf = reinterpret_cast<const float*>(smem + L.raw + s * stage_bytes);
+      const float* Yf = Hf + p.KC * us2;
+      char* hi = smem + L.ops + 2 * b * L.opb;
+      char* lo = hi + L.opb;
+      const int nq = 2 * ((cd.nrows + 7) >> 3);  // k-quads incl. zero padding to K%8
+      const int ntask = MBr * nq;
+      for (int task = ct; task < ntask; task += TC_CONV) {
+        const int qd = task / MBr;
+        const int f = task - qd * MBr;
+        float x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = 4 * qd + i;
+          float v = 0.f;
+          if (k < cd.nrows) {
+            if (f < 2 * UP) {
+              if (f < us2) v = Hf[k * us2 + f];
+            } else if (f < MU) {
+              const int t = (f - 2 * UP) >> 1;
+              v = Yf[(t * p.KCP + k) * 2 + (f & 1)];
+            }
+          }
+          x[i] = v;
+        }
+        float4 h, l;
+        h.x = __uint_as_float(__float_as_uint(x[0]) & 0xffffe000u);
+        h.y = __uint_as_float(__float_as_uint(x[1]) & 0xffffe000u);
+        h.z = __uint_as_float(__float_as_uint(x[2]) & 0xffffe000u);
+        h.w = __uint_as_float(__float_as_uint(x[3]) & 0xffffe000u);
+        l.x = x[0] - h.x;
+        l.y = x[1] - h.y;
+        l.z = x[2] - h.z;
+        l.w = x[3] - h.w;
+        const int off = (f >> 3) * 1024 + qd * 128 + (f & 7) * 16;
+        *reinterpret_cast<float4*>(hi + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = l;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&op_full[b]);
+      mbar_arrive(&raw_empty[s]);
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1u;
+      }
+      if (++j == p.nchunks) j = 0;
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue ----
+    const Team<TC_EPI, 1> tm{tid - (TC_THREADS - TC_EPI)};
+    const int wq = warp & 3;
+    const int m = 32 * wq + lane;  // accumulator row owned by this thread
+    const bool odd = (m & 1) != 0;
+    float* Gf = reinterpret_cast<float*>(w.G);
+    float* Zf = reinterpret_cast<float*>(w.Z);
+    const int LD = w.LD;
+    int j = 0, unit = 0, cl_first = 1;
+    int64_t n = blockIdx.x;
+    for (int q = 0; q < total; ++q) {
+      const ChunkDesc cd = p.chunks[j];
+      const int64_t n_cur = n;
+      if (++j == p.nchunks) {
+        j = 0;
+        n += gridDim.x;
+      }
+      const bool item_end = (cd.flags & CH_ITEM_END) != 0;
+      const bool unit_end = item_end || (per_cluster && (cd.flags & CH_CLUSTER_END));
+      if (!unit_end) continue;
+      const int a = unit & 1;
+      mbar_wait(&acc_full[a], (uint32_t)((unit >> 1) & 1));
+      tc_fence_after();
+      float v[N];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * N);
+#pragma unroll
+      for (int h = 0; h < N / 16; ++h) {
+        float t16[16];
+        tmem_ld16(taddr + 16 * h, t16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[16 * h + i] = t16[i];
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[a]);
+      // partner row (m ^ 1) holds the other component of the same complex row
+#pragma unroll
+      for (int c = 0; c < UP; ++c) {
+        const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
+        if (m < 2 * UP) {
+          const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
+          Gf[((m >> 1) * LD + c) * 2 + (odd ? 1 : 0)] = val;
+        } else if (m < MU) {
+          const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
+          Zf[(((m - 2 * UP) >> 1) * LD + c) * 2 + (odd ? 1 : 0)] = val;
+        }
+      }
+      tm.sync();
+      unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
+      tm.sync();
+      ++unit;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace dbp
