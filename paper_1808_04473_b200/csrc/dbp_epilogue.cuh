@@ -125,17 +125,20 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     return;
   }
   const float rho = (a.kind == EQ_LMMSE) ? a.n0 / a.es : 0.f;
+  // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows
+  constexpr int RS = (NT >= UP) ? NT / UP : 1;
   constexpr int EPT = (UP * UP + NT - 1) / NT;
+  const int j = tid % UP;
+  const int i0 = tid / UP;
   float2 m[EPT];
   float2* rowb = w.W;           // [2][UP] pivot rows (double-buffered)
   float2* colb = w.W + 2 * UP;  // [2][UP] pivot columns
   const float tolf = 8.f * (float)u * FLT_EPSILON;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
-    const int e = tid + r * NT;
-    const int i = e / UP, j = e % UP;
+    const int i = i0 + r * RS;
     float2 v = make_float2(0.f, 0.f);
-    if (e < UP * UP && i < u && j < u) {
+    if (i < u && j < u) {
       v = w.G[i * LD + j];
       if (i == j) {
         v.x += rho;
@@ -145,14 +148,14 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     }
     m[r] = v;
   }
+  const bool live = (i0 < UP);  // threads beyond UP*UP elements (NT > UP*UP) idle
   for (int k = 0; k < u; ++k) {
     float2* rk = rowb + (k & 1) * UP;
     float2* ck = colb + (k & 1) * UP;
+    if (live) {
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      const int e = tid + r * NT;
-      const int i = e / UP, j = e % UP;
-      if (e < UP * UP) {
+      for (int r = 0; r < EPT; ++r) {
+        const int i = i0 + r * RS;
         if (i == k) rk[j] = m[r];
         if (j == k) ck[i] = m[r];
       }
@@ -164,39 +167,58 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
       p = 1.f;
     }
     const float rp = 1.f / p;
+    if (live) {
+      const float2 rkj = c_scale(rk[j], rp);
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      const int e = tid + r * NT;
-      if (e < UP * UP) {
-        const int i = e / UP, j = e % UP;
+      for (int r = 0; r < EPT; ++r) {
+        const int i = i0 + r * RS;
         if (i == k) {
           m[r] = (j == k) ? make_float2(rp, 0.f) : c_scale(m[r], rp);
         } else if (j == k) {
           m[r] = c_scale(m[r], -rp);
         } else {
-          c_fms(m[r], c_scale(ck[i], rp), rk[j]);
+          c_fms(m[r], ck[i], rkj);
         }
       }
     }
   }
+  if (live) {
 #pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int e = tid + r * NT;
-    const int i = e / UP, j = e % UP;
-    if (e < UP * UP && i < u && j < u) w.G[i * LD + j] = m[r];
+    for (int r = 0; r < EPT; ++r) {
+      const int i = i0 + r * RS;
+      if (i < u && j < u) w.G[i * LD + j] = m[r];
+    }
   }
   tm.sync();
-  // z = A y_mrc per OFDM symbol (+ unbiasing), variances from diag(A)
+  // z = A y_mrc per OFDM symbol (+ unbiasing), two symbols per thread sharing
+  // the A row; rows are 16-byte aligned (LD even) -> float4 loads
   const bool unb = (a.kind == EQ_LMMSE) && a.unbias;
-  for (int e = tid; e < T * u; e += NT) {
-    const int t = e / u, i = e - t * u;
+  const int th = (T + 1) / 2;
+  for (int e = tid; e < th * u; e += NT) {
+    const int t0 = e / u, i = e - t0 * u;
+    const int t1 = t0 + th;
     const float2* arow = w.G + i * LD;
-    const float2* zrow = w.Z + t * LD;
-    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int j = 0; j < u; ++j) c_fma(acc, arow[j], zrow[j]);
-    if (unb) acc = c_scale(acc, 1.f / (1.f - rho * arow[i].x));
-    w.X[t * LD + i] = acc;
+    const float2* z0 = w.Z + t0 * LD;
+    const float2* z1 = w.Z + (t1 < T ? t1 : t0) * LD;
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+    for (int jj = 0; jj < u; jj += 2) {
+      const float4 av = *reinterpret_cast<const float4*>(arow + jj);
+      const float4 b0 = *reinterpret_cast<const float4*>(z0 + jj);
+      const float4 b1 = *reinterpret_cast<const float4*>(z1 + jj);
+      c_fma(acc0, make_float2(av.x, av.y), make_float2(b0.x, b0.y));
+      c_fma(acc1, make_float2(av.x, av.y), make_float2(b1.x, b1.y));
+      if (jj + 1 < u) {
+        c_fma(acc0, make_float2(av.z, av.w), make_float2(b0.z, b0.w));
+        c_fma(acc1, make_float2(av.z, av.w), make_float2(b1.z, b1.w));
+      }
+    }
+    if (unb) {
+      const float rc = 1.f / (1.f - rho * arow[i].x);
+      acc0 = c_scale(acc0, rc);
+      acc1 = c_scale(acc1, rc);
+    }
+    w.X[t0 * LD + i] = acc0;
+    if (t1 < T) w.X[t1 * LD + i] = acc1;
   }
   for (int i = tid; i < u; i += NT) {
     const float aii = w.G[i * LD + i].x;

@@ -219,6 +219,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   if (2 * UP + 2 * p.T > 128) return fail(DBP_E_UNSUPPORTED, "2(U+T) > 128 on the tensor-core path");
+  p.NS = 3;
   const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd);
   auto kern = tc_kernel<UP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)

@@ -17,7 +17,7 @@ struct WorkLayout {
 
 __host__ __device__ inline WorkLayout make_work_layout(int base, int UP, int TP, int C, bool lama, bool fd) {
   WorkLayout L;
-  const int LD = UP + 1;
+  const int LD = UP + 2;  // even: 16-byte aligned rows for float4 access
   const int V = (UP > TP ? UP : TP);
   int o = align_up(base, 16);
   L.G = o;
@@ -80,7 +80,7 @@ __device__ __forceinline__ Work make_work(char* smem, const WorkLayout& L, int U
   w.harm = reinterpret_cast<float*>(smem + L.harm);
   w.wbuf = reinterpret_cast<float*>(smem + L.wbuf);
   w.flags = reinterpret_cast<int*>(smem + L.flags);
-  w.LD = UP + 1;
+  w.LD = UP + 2;
   return w;
 }
 

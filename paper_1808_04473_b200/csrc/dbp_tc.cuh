@@ -56,17 +56,19 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int st
   L.ops = o;
   L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
   o += 4 * L.opb;     // [hi0][lo0][hi1][lo1]
-  // the M=128 MMA reads 16 blocks from each tile base; rows past MB*8 are
-  // never written and only produce ignored accumulator rows
-  L.slack = (16 - MB) * 1024;
-  o += L.slack;
   L.w = make_work_layout(o, UP, TP, C, lama, fd);
+  // the M=128 MMA reads 16 blocks (16 KB) from each tile base; rows past
+  // MB*8 are never written and only produce ignored accumulator rows, but
+  // they must stay inside the CTA's shared memory
+  const int after_last = L.w.total - (o - L.opb);
+  L.slack = (after_last < 16 * 1024) ? 16 * 1024 - after_last : 0;
+  L.w.total += L.slack;
   L.total = L.w.total;
   return L;
 }
 
 template <int UP>
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p) {
+__global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(1024) char smem[];
   constexpr int N = 2 * UP;
   constexpr uint32_t TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
@@ -182,9 +184,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(const __grid_constant
     __syncwarp();
   } else if (warp < 4) {
     // -------------------------------------------------------- converters ----
+    // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
+    // Tile layout: feature f, antenna k -> (f/8)*1024 + (k/4)*128 + (f%8)*16
+    // + (k%4)*4 bytes.  H tasks move a 4-feature x 4-antenna block (4x4
+    // transpose in registers), Y tasks one symbol's (re, im) rows x 4 antennas.
     const int ct = tid - 64;
-    const int MBr = MB * 8;
     const int us2 = 2 * p.us;
+    constexpr int HG = UP / 2;  // 4-feature groups of the H part
+    // rows between 2(U+T) and MB*8 are zero forever (A padding rows)
+    for (int e = ct; e < 4 * (MB * 8 - MU) * 8; e += TC_CONV) {
+      const int per_buf = (MB * 8 - MU) * 8;
+      const int buf = e / per_buf, r = e % per_buf;
+      const int f = MU + r / 8, qd = r % 8;
+      *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + (f >> 3) * 1024 + qd * 128 + (f & 7) * 16) =
+          make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    auto split = [](float x, float& h, float& l) {
+      h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+      l = x - h;
+    };
     int j = 0, s = 0;
     uint32_t ph = 0;
     for (int q = 0; q < total; ++q) {
@@ -196,38 +214,69 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(const __grid_constant
       const float* Yf = Hf + p.KC * us2;
       char* hi = smem + L.ops + 2 * b * L.opb;
       char* lo = hi + L.opb;
-      const int nq = 2 * ((cd.nrows + 7) >> 3);  // k-quads incl. zero padding to K%8
-      const int ntask = MBr * nq;
+      const int nr = cd.nrows;
+      const int nq = 2 * ((nr + 7) >> 3);  // k-quads incl. zero padding to K % 8
+      const bool full = (nr & 7) == 0;
+      const int ntask = (HG + p.T) * nq;
       for (int task = ct; task < ntask; task += TC_CONV) {
-        const int qd = task / MBr;
-        const int f = task - qd * MBr;
-        float x[4];
+        const int qd = task / (HG + p.T);
+        const int g = task - qd * (HG + p.T);
+        const int k0 = 4 * qd;
+        if (g < HG) {
+          const int f0 = 4 * g;
+          float4 r[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = 4 * qd + i;
-          float v = 0.f;
-          if (k < cd.nrows) {
-            if (f < 2 * UP) {
-              if (f < us2) v = Hf[k * us2 + f];
-            } else if (f < MU) {
-              const int t = (f - 2 * UP) >> 1;
-              v = Yf[(t * p.KCP + k) * 2 + (f & 1)];
-            }
+          for (int i = 0; i < 4; ++i) {
+            const int k = k0 + i;
+            r[i] = (f0 < us2 && (full || k < nr)) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          x[i] = v;
+          const float c0[4] = {r[0].x, r[1].x, r[2].x, r[3].x};
+          const float c1[4] = {r[0].y, r[1].y, r[2].y, r[3].y};
+          const float c2[4] = {r[0].z, r[1].z, r[2].z, r[3].z};
+          const float c3[4] = {r[0].w, r[1].w, r[2].w, r[3].w};
+          const float* cols[4] = {c0, c1, c2, c3};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int f = f0 + c;
+            float4 h, l;
+            split(cols[c][0], h.x, l.x);
+            split(cols[c][1], h.y, l.y);
+            split(cols[c][2], h.z, l.z);
+            split(cols[c][3], h.w, l.w);
+            const int off = (f >> 3) * 1024 + qd * 128 + (f & 7) * 16;
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+          }
+        } else {
+          const int t = g - HG;
+          const float* yr = Yf + (t * p.KCP + k0) * 2;  // 4 complex = 2 float4
+          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+          if (full || k0 + 3 < nr) {
+            a0 = *reinterpret_cast<const float4*>(yr);
+            a1 = *reinterpret_cast<const float4*>(yr + 4);
+          } else {
+            if (k0 < nr) { a0.x = yr[0]; a0.y = yr[1]; }
+            if (k0 + 1 < nr) { a0.z = yr[2]; a0.w = yr[3]; }
+            if (k0 + 2 < nr) { a1.x = yr[4]; a1.y = yr[5]; }
+          }
+          const int fr = 2 * UP + 2 * t;
+          float4 h, l;
+          split(a0.x, h.x, l.x);
+          split(a0.z, h.y, l.y);
+          split(a1.x, h.z, l.z);
+          split(a1.z, h.w, l.w);
+          int off = (fr >> 3) * 1024 + qd * 128 + (fr & 7) * 16;
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = l;
+          split(a0.y, h.x, l.x);
+          split(a0.w, h.y, l.y);
+          split(a1.y, h.z, l.z);
+          split(a1.w, h.w, l.w);
+          off += 16;  // fr even -> fr + 1 shares the core-matrix block
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = l;
         }
-        float4 h, l;
-        h.x = __uint_as_float(__float_as_uint(x[0]) & 0xffffe000u);
-        h.y = __uint_as_float(__float_as_uint(x[1]) & 0xffffe000u);
-        h.z = __uint_as_float(__float_as_uint(x[2]) & 0xffffe000u);
-        h.w = __uint_as_float(__float_as_uint(x[3]) & 0xffffe000u);
-        l.x = x[0] - h.x;
-        l.y = x[1] - h.y;
-        l.z = x[2] - h.z;
-        l.w = x[3] - h.w;
-        const int off = (f >> 3) * 1024 + qd * 128 + (f & 7) * 16;
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = l;
       }
       fence_proxy_async_smem();
       mbar_arrive(&op_full[b]);
@@ -262,29 +311,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(const __grid_constant
       const int a = unit & 1;
       mbar_wait(&acc_full[a], (uint32_t)((unit >> 1) & 1));
       tc_fence_after();
-      float v[N];
       const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * N);
+      // 16 accumulator columns = 8 UE columns (re, im) per tcgen05.ld; the
+      // partner row (m ^ 1) holds the other component of the same complex row
 #pragma unroll
       for (int h = 0; h < N / 16; ++h) {
-        float t16[16];
-        tmem_ld16(taddr + 16 * h, t16);
+        float v[16];
+        tmem_ld16(taddr + 16 * h, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[16 * h + i] = t16[i];
+        for (int c = 0; c < 8; ++c) {
+          const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
+          const int col = 8 * h + c;
+          if (m < 2 * UP) {
+            const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
+            Gf[((m >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+          } else if (m < MU) {
+            const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
+            Zf[(((m - 2 * UP) >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+          }
+        }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[a]);
-      // partner row (m ^ 1) holds the other component of the same complex row
-#pragma unroll
-      for (int c = 0; c < UP; ++c) {
-        const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
-        if (m < 2 * UP) {
-          const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
-          Gf[((m >> 1) * LD + c) * 2 + (odd ? 1 : 0)] = val;
-        } else if (m < MU) {
-          const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
-          Zf[(((m - 2 * UP) >> 1) * LD + c) * 2 + (odd ? 1 : 0)] = val;
-        }
-      }
       tm.sync();
       unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
       tm.sync();

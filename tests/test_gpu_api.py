@@ -374,15 +374,21 @@ class TestFdPipeline:
         for c in (1, 2, 4, 8):
             part = ClusterPartition.uniform(64, c)
             ch = dbp.ChannelRealization(g[f"fd{c}_h"], part)
+            # fp32 error grows with the local condition number (square local
+            # systems, B_c = U = 16 at C = 4, reach kappa(G_c) ~ 4e4): tolerance
+            # max(1e-4, 2e-6 kappa_max) -- the BASELINE configs have kappa ~ 20
+            hh = g[f"fd{c}_h"]
+            kappa = max(np.linalg.cond(hh[sl].conj().T @ hh[sl]) for sl in part.slices())
+            tol = max(1e-4, 2e-6 * kappa)
             for kind in ("mrc", "zf", "lmmse", "lama"):
                 if f"fd{c}_{kind}_z" not in g:
                     continue
                 lp = {"t_max": 5} if kind == "lama" else None
                 fd = dbp.fd_equalize(kind, ch, g[f"fd{c}_y"], 0.1, constellation=QAM16, lama_params=lp,
                                      return_weights=True)
-                assert rel(fd.z, g[f"fd{c}_{kind}_z"]) < 1e-4, (c, kind)
-                assert rel(fd.sigma2, g[f"fd{c}_{kind}_sigma2"]) < 1e-4, (c, kind)
-                assert rel(fd.nu, g[f"fd{c}_{kind}_nu"]) < 1e-4, (c, kind)
+                assert rel(fd.z, g[f"fd{c}_{kind}_z"]) < tol, (c, kind)
+                assert rel(fd.sigma2, g[f"fd{c}_{kind}_sigma2"]) < tol, (c, kind)
+                assert rel(fd.nu, g[f"fd{c}_{kind}_nu"]) < tol, (c, kind)
 
     def test_mrc_fd_equals_pd_exactly(self):
         for c in (1, 2, 4, 8):
