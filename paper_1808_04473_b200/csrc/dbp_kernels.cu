@@ -220,15 +220,21 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   if (2 * UP + 2 * p.T > 128) return fail(DBP_E_UNSUPPORTED, "2(U+T) > 128 on the tensor-core path");
   p.NS = 3;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd);
+  int dev = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // as many solver warps as shared memory allows (one unit working set each)
+  int nsolv = TC_MAX_SOLV;
+  while (nsolv > 1 && make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd, nsolv).total > smem_max)
+    --nsolv;
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd, nsolv);
+  if (L.total > smem_max) return fail(DBP_E_UNSUPPORTED, "tensor-core kernel does not fit in shared memory");
   auto kern = tc_kernel<UP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TC_THREADS, L.total);
-  if (per_sm < 1) return fail(DBP_E_UNSUPPORTED, "kernel does not fit on an SM");
-  const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count() * per_sm);
-  kern<<<(unsigned)grid, TC_THREADS, L.total, st>>>(p);
+  const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
+  const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count());
+  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv);
   return cuda_check("tc_kernel");
 }
 

@@ -12,41 +12,69 @@
 // split (x = hi + lo, P = hi.hi + hi.lo + lo.hi) so the result keeps fp32
 // accuracy (plain TF32 would miss the 1e-4 tolerance: SURVEY.md 8(c)).
 //
-// Roles (8 warps):
-//   warp 0      TMA producer: bulk copies of each chunk (<= 32 antenna rows
-//               of one cluster) of H and Y into a ring of raw stages
-//   warp 1      MMA issuer (one thread): 3 x ceil(rows/8) tcgen05.mma per
-//               chunk into one of two TMEM accumulator slots
-//   warps 2-3   converters: raw stage -> hi/lo operand tiles in the canonical
-//               K-major core-matrix layout (8 rows x 16 B per core matrix)
-//   warps 4-7   epilogue: tcgen05.ld the accumulator (warp w owns TMEM lanes
-//               32(w%4)..+31), assemble G / y_mrc, then the unit epilogue
-//               (solve, FD fusion, stores) on a named barrier
-// Everything is pipelined through mbarriers, so the loads and MMAs of the
-// next units overlap the epilogue of the current one.
+// Roles (one persistent CTA per SM):
+//   warp 0       TMA producer: bulk copies of each chunk (<= 32 antenna rows
+//                of one cluster) of H and Y into a ring of raw stages
+//   warp 1       MMA issuer (one thread): 3 x ceil(rows/8) tcgen05.mma per
+//                chunk into one of two TMEM accumulator slots
+//   warps 2-5    converters: raw stage -> hi/lo operand tiles in the canonical
+//                K-major core-matrix layout (8 rows x 16 B per core matrix)
+//   warps 6-9    assemblers: tcgen05.ld of the accumulator (warp w owns TMEM
+//                lanes 32(w%4)..+31), G / y_mrc written into a solver's slot
+//   warps 10..   solvers: one warp per unit (round robin), the whole unit
+//                epilogue (solve, outputs) with __syncwarp only; FD units of
+//                one item are folded into an item ring in cluster order
+// Everything is pipelined through mbarriers: loads, conversions and MMAs of
+// later units overlap the solves of earlier ones, and several units are
+// solved concurrently.
 #pragma once
 #include "dbp_simt.cuh"
 
 namespace dbp {
 
-constexpr int TC_THREADS = 256;
-constexpr int TC_CONV = 64;   // converter threads (warps 2-3)
-constexpr int TC_EPI = 128;   // epilogue threads (warps 4-7)
-constexpr int TC_OPB_K = 32;  // antenna rows per operand tile (= KC)
+constexpr int TC_CONV_W = 4;  // converter warps (2..5)
+constexpr int TC_ASM_W = 4;   // assembler warps (6..9)
+constexpr int TC_FIRST_SOLVER = 2 + TC_CONV_W + TC_ASM_W;
+constexpr int TC_MAX_SOLV = 6;
+constexpr int TC_CONV = 32 * TC_CONV_W;
+constexpr int TC_ASM = 32 * TC_ASM_W;
+constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
+
+// FD item ring slot: the fusion sums of one item, folded cluster by cluster.
+struct ItemSlotLayout {
+  int num, den, harm, wbuf, flags, total;
+};
+
+__host__ __device__ inline ItemSlotLayout make_item_slot(int UP, int TP, int C) {
+  ItemSlotLayout S;
+  const int LD = UP + 2, V = (UP > TP ? UP : TP);
+  int o = 0;
+  S.num = o;
+  o += TP * LD * 8;
+  S.den = o;
+  o += V * 4;
+  S.harm = o;
+  o += V * 4;
+  S.wbuf = o;
+  o += C * V * 4;
+  S.flags = o;
+  o += 16;  // [0] status, [1] divergence iteration, [2] turn counter
+  S.total = align_up(o, 128);
+  return S;
+}
 
 struct TcLayout {
-  int bars, tmem_slot, raw, ops, opb, slack;
-  WorkLayout w;
-  int total;
+  int bars, tmem_slot, raw, ops, opb, slack, work, work_stride, items, item_stride, nir, total;
+  WorkLayout w;  // offsets relative to a solver's work base
 };
 
 __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int stage_bytes, int NS, int C, bool lama,
-                                                   bool fd) {
+                                                   bool fd, int nsolv) {
   TcLayout L;
   const int MB = (2 * UP + 2 * T + 7) / 8;  // 8-row core-matrix blocks used
   int o = 0;
   L.bars = o;
-  o += (2 * NS + 8) * 8;
+  o += (2 * NS + 8 + 2 * TC_MAX_SOLV) * 8;
   L.tmem_slot = o;
   o += 16;
   o = align_up(o, 128);
@@ -56,19 +84,140 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int st
   L.ops = o;
   L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
   o += 4 * L.opb;     // [hi0][lo0][hi1][lo1]
-  L.w = make_work_layout(o, UP, TP, C, lama, fd);
+  L.work = o;
+  L.w = make_work_layout(0, UP, TP, C, lama, false);
+  L.work_stride = L.w.total;
+  o += nsolv * L.work_stride;
+  L.items = o;
+  const ItemSlotLayout S = make_item_slot(UP, TP, C);
+  L.item_stride = S.total;
+  L.nir = fd ? (nsolv + C - 1) / C + 2 : 0;
+  o += L.nir * L.item_stride;
   // the M=128 MMA reads 16 blocks (16 KB) from each tile base; rows past
   // MB*8 are never written and only produce ignored accumulator rows, but
   // they must stay inside the CTA's shared memory
-  const int after_last = L.w.total - (o - L.opb);
+  const int after_last = o - (L.work - L.opb);
   L.slack = (after_last < 16 * 1024) ? 16 * 1024 - after_last : 0;
-  L.w.total += L.slack;
-  L.total = L.w.total;
+  o += L.slack;
+  L.total = align_up(o, 128);
   return L;
 }
 
+__device__ __forceinline__ Work work_at(char* smem, const TcLayout& L, int sv, int UP) {
+  WorkLayout wl = L.w;
+  const int base = L.work + sv * L.work_stride;
+  wl.G += base;
+  wl.Z += base;
+  wl.X += base;
+  wl.W += base;
+  wl.Sv += base;
+  wl.Vv += base;
+  wl.Fb += base;
+  wl.gb += base;
+  wl.num += base;
+  wl.phi += base;
+  wl.coef += base;
+  wl.s2 += base;
+  wl.gn += base;
+  wl.dg += base;
+  wl.den += base;
+  wl.harm += base;
+  wl.wbuf += base;
+  wl.flags += base;
+  return make_work(smem, wl, UP);
+}
+
+// FD: fold one solved cluster into its item's ring slot, strictly in cluster
+// order (deterministic sums; a solver waits for its turn), and finalize the
+// item on its last cluster (fusion.py:141-154).  Runs on one warp.
+template <int UP, class TM>
+__device__ void fd_fold(const Work& w, char* slot, const ItemSlotLayout& S, const EqParams& p, int64_t n, int il,
+                        int c, int nir, const TM& tm) {
+  const int u = p.u, T = p.T, LD = w.LD, C = p.C;
+  const bool lama = p.kind == EQ_LAMA;
+  const int wdim = lama ? T : u;
+  float2* num = reinterpret_cast<float2*>(slot + S.num);
+  float* den = reinterpret_cast<float*>(slot + S.den);
+  float* harm = reinterpret_cast<float*>(slot + S.harm);
+  float* wbuf = reinterpret_cast<float*>(slot + S.wbuf);
+  int* flags = reinterpret_cast<int*>(slot + S.flags);
+  volatile int* turn = flags + 2;
+  const int key = il * C + c;
+  if (tm.t == 0) {
+    while (*turn != key) __nanosleep(32);
+  }
+  tm.sync();
+  __threadfence_block();
+  const bool first = (c == 0);
+  for (int e = tm.t; e < wdim; e += TM::N) {
+    const float s2 = w.s2[e];
+    if (p.kind != EQ_MRC && !(s2 > 0.f)) set_status(w.flags, ST_BADVAR);
+    const float inv = 1.f / fmaxf(s2, VAR_FLOOR);
+    const float wt = (p.kind == EQ_MRC) ? w.gn[e] : inv;
+    wbuf[c * wdim + e] = wt;
+    den[e] = first ? wt : den[e] + wt;
+    harm[e] = first ? inv : harm[e] + inv;
+  }
+  for (int e = tm.t; e < T * u; e += TM::N) {
+    const int t = e / u, i = e - t * u;
+    const int k = lama ? t : i;
+    const float s2 = w.s2[k];
+    const float wt = (p.kind == EQ_MRC) ? w.gn[k] : 1.f / fmaxf(s2, VAR_FLOOR);
+    const float2 x = c_scale(w.X[t * LD + i], wt);
+    num[t * LD + i] = first ? x : c_add(num[t * LD + i], x);
+  }
+  tm.sync();
+  if (tm.t == 0) {
+    if (first) {
+      flags[0] = 0;
+      flags[1] = 0x7fffffff;
+    }
+    if (w.flags[0] && flags[0] == 0) flags[0] = w.flags[0];
+    if (w.flags[1] < flags[1]) flags[1] = w.flags[1];
+  }
+  if (c == C - 1) {
+    tm.sync();
+    __threadfence_block();
+    if (p.arch == ARCH_FD) {
+      for (int e = tm.t; e < T * u; e += TM::N) {
+        const int t = e / u, i = e - t * u;
+        const float2 x = c_scale(num[t * LD + i], 1.f / den[lama ? t : i]);
+        const size_t o = ((size_t)n * T + t) * u + i;
+        p.xhat[o] = x;
+        if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+      }
+      for (int e = tm.t; e < wdim; e += TM::N) p.sigma2[(size_t)n * wdim + e] = 1.f / harm[e];
+      if (p.nu)
+        for (int e = tm.t; e < C * wdim; e += TM::N) p.nu[(size_t)n * C * wdim + e] = wbuf[e] / den[e % wdim];
+    } else {  // FD_PARTIAL: raw sums for a cross-GPU reduction
+      const int rec = 2 * T * u + 2 * wdim;
+      float* dst = p.fd_acc + (size_t)n * rec;
+      for (int e = tm.t; e < T * u; e += TM::N) {
+        const int t = e / u, i = e - t * u;
+        const float2 v = num[t * LD + i];
+        dst[2 * e] = v.x;
+        dst[2 * e + 1] = v.y;
+      }
+      for (int e = tm.t; e < wdim; e += TM::N) {
+        dst[2 * T * u + e] = den[e];
+        dst[2 * T * u + wdim + e] = harm[e];
+      }
+      for (int e = tm.t; e < C * wdim; e += TM::N) p.fd_wraw[(size_t)n * C * wdim + e] = wbuf[e];
+    }
+    if (tm.t == 0) {
+      int st = flags[0];
+      if (flags[1] < 0x7fffffff) st = st ? st : ST_DIVERGED;
+      p.status[n] = st;
+      if (p.iters) p.iters[n] = (flags[1] < 0x7fffffff) ? flags[1] : 0;
+    }
+  }
+  tm.sync();
+  __threadfence_block();
+  if (tm.t == 0) *turn = (c == C - 1) ? (il + nir) * C : key + 1;
+}
+
 template <int UP>
-__global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant__ EqParams p) {
+__global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv) {
   extern __shared__ __align__(1024) char smem[];
   constexpr int N = 2 * UP;
   constexpr uint32_t TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
@@ -79,15 +228,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
   const int MU = 2 * UP + 2 * p.T;
   const int MB = (MU + 7) / 8;
   const int stage_bytes = p.stage_f2 * 8;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, stage_bytes, NS, p.C, lama, fd);
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, stage_bytes, NS, p.C, lama, fd, nsolv);
+  const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* raw_empty = raw_full + NS;
   uint64_t* op_full = raw_empty + NS;
   uint64_t* op_empty = op_full + 2;
   uint64_t* acc_full = op_empty + 2;
   uint64_t* acc_empty = acc_full + 2;
+  uint64_t* slot_full = acc_empty + 2;
+  uint64_t* slot_empty = slot_full + TC_MAX_SOLV;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
-  const Work w = make_work(smem, L.w, UP);
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -98,15 +249,21 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
       mbar_init(&op_full[b], TC_CONV);
       mbar_init(&op_empty[b], 1);
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], TC_EPI);
+      mbar_init(&acc_empty[b], TC_ASM);
+    }
+    for (int v = 0; v < nsolv; ++v) {
+      mbar_init(&slot_full[v], TC_ASM);
+      mbar_init(&slot_empty[v], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
-  if (tid == TC_THREADS - TC_EPI) {
-    w.flags[0] = 0;
-    w.flags[1] = 0x7fffffff;
+  for (int k = tid; k < L.nir; k += blockDim.x) {
+    int* f = reinterpret_cast<int*>(smem + L.items + k * L.item_stride + IS.flags);
+    f[0] = 0;
+    f[1] = 0x7fffffff;
+    f[2] = k * p.C;  // turn: first cluster of CTA-local item k
   }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -182,7 +339,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
+  } else if (warp < 2 + TC_CONV_W) {
     // -------------------------------------------------------- converters ----
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
     // Tile layout: feature f, antenna k -> (f/8)*1024 + (k/4)*128 + (f%8)*16
@@ -205,6 +362,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
     };
     int j = 0, s = 0;
     uint32_t ph = 0;
+    const int ng = HG + p.T;
     for (int q = 0; q < total; ++q) {
       const int b = q & 1;
       mbar_wait(&raw_full[s], ph);
@@ -217,10 +375,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
       const int nr = cd.nrows;
       const int nq = 2 * ((nr + 7) >> 3);  // k-quads incl. zero padding to K % 8
       const bool full = (nr & 7) == 0;
-      const int ntask = (HG + p.T) * nq;
+      const int ntask = ng * nq;
       for (int task = ct; task < ntask; task += TC_CONV) {
-        const int qd = task / (HG + p.T);
-        const int g = task - qd * (HG + p.T);
+        const int qd = task / ng;
+        const int g = task - qd * ng;
         const int k0 = 4 * qd;
         if (g < HG) {
           const int f0 = 4 * g;
@@ -256,9 +414,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
             a0 = *reinterpret_cast<const float4*>(yr);
             a1 = *reinterpret_cast<const float4*>(yr + 4);
           } else {
-            if (k0 < nr) { a0.x = yr[0]; a0.y = yr[1]; }
-            if (k0 + 1 < nr) { a0.z = yr[2]; a0.w = yr[3]; }
-            if (k0 + 2 < nr) { a1.x = yr[4]; a1.y = yr[5]; }
+            if (k0 < nr) {
+              a0.x = yr[0];
+              a0.y = yr[1];
+            }
+            if (k0 + 1 < nr) {
+              a0.z = yr[2];
+              a0.w = yr[3];
+            }
+            if (k0 + 2 < nr) {
+              a1.x = yr[4];
+              a1.y = yr[5];
+            }
           }
           const int fr = 2 * UP + 2 * t;
           float4 h, l;
@@ -287,56 +454,104 @@ __global__ void __launch_bounds__(TC_THREADS, 2) tc_kernel(const __grid_constant
       }
       if (++j == p.nchunks) j = 0;
     }
-  } else {
-    // ---------------------------------------------------------- epilogue ----
-    const Team<TC_EPI, 1> tm{tid - (TC_THREADS - TC_EPI)};
-    const int wq = warp & 3;
+  } else if (warp < TC_FIRST_SOLVER) {
+    // -------------------------------------------------------- assemblers ----
+    const int wq = warp & 3;       // TMEM lane quarter this warp may access
     const int m = 32 * wq + lane;  // accumulator row owned by this thread
     const bool odd = (m & 1) != 0;
-    float* Gf = reinterpret_cast<float*>(w.G);
-    float* Zf = reinterpret_cast<float*>(w.Z);
-    const int LD = w.LD;
-    int j = 0, unit = 0, cl_first = 1;
-    int64_t n = blockIdx.x;
+    const bool has_rows = 32 * wq < MU;
+    int j = 0, unit = 0;
     for (int q = 0; q < total; ++q) {
       const ChunkDesc cd = p.chunks[j];
-      const int64_t n_cur = n;
-      if (++j == p.nchunks) {
-        j = 0;
-        n += gridDim.x;
-      }
-      const bool item_end = (cd.flags & CH_ITEM_END) != 0;
-      const bool unit_end = item_end || (per_cluster && (cd.flags & CH_CLUSTER_END));
+      if (++j == p.nchunks) j = 0;
+      const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
       if (!unit_end) continue;
+      const int sv = unit % nsolv;
+      if (unit >= nsolv) mbar_wait(&slot_empty[sv], (uint32_t)(((unit / nsolv) - 1) & 1));
       const int a = unit & 1;
       mbar_wait(&acc_full[a], (uint32_t)((unit >> 1) & 1));
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * N);
-      // 16 accumulator columns = 8 UE columns (re, im) per tcgen05.ld; the
-      // partner row (m ^ 1) holds the other component of the same complex row
+      if (has_rows) {
+        const Work w = work_at(smem, L, sv, UP);
+        float* Gf = reinterpret_cast<float*>(w.G);
+        float* Zf = reinterpret_cast<float*>(w.Z);
+        const int LD = w.LD;
+        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * N);
+        // 16 accumulator columns = 8 UE columns (re, im) per tcgen05.ld; the
+        // partner row (m ^ 1) holds the other component of the same complex row
 #pragma unroll
-      for (int h = 0; h < N / 16; ++h) {
-        float v[16];
-        tmem_ld16(taddr + 16 * h, v);
+        for (int h = 0; h < N / 16; ++h) {
+          float v[16];
+          tmem_ld16(taddr + 16 * h, v);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
-          const int col = 8 * h + c;
-          if (m < 2 * UP) {
-            const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
-            Gf[((m >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
-          } else if (m < MU) {
-            const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
-            Zf[(((m - 2 * UP) >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+          for (int c = 0; c < 8; ++c) {
+            const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
+            const int col = 8 * h + c;
+            if (m < 2 * UP) {
+              const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
+              Gf[((m >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+            } else if (m < MU) {
+              const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
+              Zf[(((m - 2 * UP) >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+            }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[a]);
-      tm.sync();
-      unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
-      tm.sync();
+      mbar_arrive(&slot_full[sv]);
       ++unit;
+    }
+  } else {
+    // ----------------------------------------------------------- solvers ----
+    const int sv = warp - TC_FIRST_SOLVER;
+    const Team<32, -1> tm{lane};
+    const Work w = work_at(smem, L, sv, UP);
+    int j = 0, unit = 0, il = 0, cl_first = 1;
+    int64_t n = blockIdx.x;
+    for (int q = 0; q < total; ++q) {
+      const ChunkDesc cd = p.chunks[j];
+      const int64_t n_cur = n;
+      const int il_cur = il;
+      if (++j == p.nchunks) {
+        j = 0;
+        n += gridDim.x;
+        ++il;
+      }
+      const bool item_end = (cd.flags & CH_ITEM_END) != 0;
+      const bool unit_end = item_end || (per_cluster && (cd.flags & CH_CLUSTER_END));
+      if (!unit_end) continue;
+      const int my = (unit % nsolv == sv);
+      const int round = unit / nsolv;
+      ++unit;
+      if (!my) continue;
+      mbar_wait(&slot_full[sv], (uint32_t)(round & 1));
+      reset_flags(w, tm);
+      tm.sync();
+      if (!fd) {
+        unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
+      } else {
+        const int c = cd.cluster;
+        EpiArgs a;
+        a.kind = p.kind;
+        a.u = p.u;
+        a.T = p.T;
+        a.n0 = item_n0(p, n_cur);
+        a.es = p.es;
+        a.damping = p.damping;
+        a.t_max = p.t_max;
+        a.beta = p.cl_beta[c];
+        a.lama_scale = p.cl_scale[c];
+        a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
+        if (lama)
+          lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
+        else
+          linear_unit<UP>(w, a, tm);
+        char* slot = smem + L.items + (il_cur % L.nir) * L.item_stride;
+        fd_fold<UP>(w, slot, IS, p, n_cur, il_cur, c, L.nir, tm);
+      }
+      tm.sync();
+      if (lane == 0) mbar_arrive(&slot_empty[sv]);
     }
   }
   tc_fence_before();
