@@ -219,22 +219,30 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   if (2 * UP + 2 * p.T > 128) return fail(DBP_E_UNSUPPORTED, "2(U+T) > 128 on the tensor-core path");
-  p.NS = 3;
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // as many solver warps as shared memory allows (one unit working set each)
+  // staging depth for ~64 KB of HBM reads in flight per SM (Little's law at
+  // ~1.5 us latency), then as many solver warps as shared memory allows
+  const int ybytes = p.T * p.B * 8;
+  int ny = ybytes <= 16384 ? 3 : 2;
+  p.NS = std::max(4, std::min(12, (64 * 1024 - ny * ybytes) / (p.KC * p.us * 8)));
+  auto fits = [&](int ns, int nyy, int nsv) {
+    return make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, ns, nyy, p.C, lama, fd, nsv).total <= smem_max;
+  };
   int nsolv = TC_MAX_SOLV;
-  while (nsolv > 1 && make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd, nsolv).total > smem_max)
-    --nsolv;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.stage_f2 * 8, p.NS, p.C, lama, fd, nsolv);
-  if (L.total > smem_max) return fail(DBP_E_UNSUPPORTED, "tensor-core kernel does not fit in shared memory");
+  while (nsolv > 2 && !fits(p.NS, ny, nsolv)) --nsolv;
+  while (p.NS > 3 && !fits(p.NS, ny, nsolv)) --p.NS;
+  while (ny > 2 && !fits(p.NS, ny, nsolv)) --ny;
+  while (nsolv > 1 && !fits(p.NS, ny, nsolv)) --nsolv;
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, p.NS, ny, p.C, lama, fd, nsolv);
+  if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
   auto kern = tc_kernel<UP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
   const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count());
-  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv);
+  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv, ny);
   return cuda_check("tc_kernel");
 }
 
@@ -259,11 +267,14 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
   static const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
   const int up = up_for(p.u);
   if (!force_simt && up <= 32 && 2 * up + 2 * p.T <= 128) {
+    int rc = 1;
     switch (up) {
-      case 8: return launch_tc<8>(p, st);
-      case 16: return launch_tc<16>(p, st);
-      case 32: return launch_tc<32>(p, st);
+      case 8: rc = launch_tc<8>(p, st); break;
+      case 16: rc = launch_tc<16>(p, st); break;
+      case 32: rc = launch_tc<32>(p, st); break;
     }
+    if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
+    p.NS = up <= 16 ? 4 : 3;
   }
   switch (up) {
     case 8: return launch_stream<8, 128>(p, st);

@@ -64,22 +64,29 @@ __host__ __device__ inline ItemSlotLayout make_item_slot(int UP, int TP, int C) 
 }
 
 struct TcLayout {
-  int bars, tmem_slot, raw, ops, opb, slack, work, work_stride, items, item_stride, nir, total;
+  int bars, tmem_slot, hst, hbytes, yst, ybytes, ops, opb, slack, work, work_stride, items, item_stride, nir, total;
   WorkLayout w;  // offsets relative to a solver's work base
 };
 
-__host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int stage_bytes, int NS, int C, bool lama,
-                                                   bool fd, int nsolv) {
+// Raw staging: a ring of NS H chunks (KC antenna rows each, one bulk copy)
+// and a ring of NY whole-item Y blocks (T x B, one bulk copy per item -- the
+// per-symbol rows of a chunk are only 8*KC bytes and would cost T tiny copies).
+__host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B, int us, int KC, int NS, int NY,
+                                                   int C, bool lama, bool fd, int nsolv) {
   TcLayout L;
   const int MB = (2 * UP + 2 * T + 7) / 8;  // 8-row core-matrix blocks used
   int o = 0;
   L.bars = o;
-  o += (2 * NS + 8 + 2 * TC_MAX_SOLV) * 8;
+  o += (2 * NS + 2 * NY + 8 + 2 * TC_MAX_SOLV) * 8;
   L.tmem_slot = o;
   o += 16;
   o = align_up(o, 128);
-  L.raw = o;
-  o += NS * stage_bytes;
+  L.hbytes = align_up(KC * us * 8, 128);
+  L.hst = o;
+  o += NS * L.hbytes;
+  L.ybytes = align_up(T * B * 8, 128);
+  L.yst = o;
+  o += NY * L.ybytes;
   o = align_up(o, 1024);
   L.ops = o;
   L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
@@ -217,7 +224,8 @@ __device__ void fd_fold(const Work& w, char* slot, const ItemSlotLayout& S, cons
 }
 
 template <int UP>
-__global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv) {
+__global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv,
+                                                                int ny) {
   extern __shared__ __align__(1024) char smem[];
   constexpr int N = 2 * UP;
   constexpr uint32_t TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
@@ -225,14 +233,16 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   const int NS = p.NS;
+  const int NY = ny;
   const int MU = 2 * UP + 2 * p.T;
   const int MB = (MU + 7) / 8;
-  const int stage_bytes = p.stage_f2 * 8;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, stage_bytes, NS, p.C, lama, fd, nsolv);
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, NS, NY, p.C, lama, fd, nsolv);
   const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // H chunk ring
   uint64_t* raw_empty = raw_full + NS;
-  uint64_t* op_full = raw_empty + NS;
+  uint64_t* y_full = raw_empty + NS;  // Y item ring
+  uint64_t* y_empty = y_full + NY;
+  uint64_t* op_full = y_empty + NY;
   uint64_t* op_empty = op_full + 2;
   uint64_t* acc_full = op_empty + 2;
   uint64_t* acc_empty = acc_full + 2;
@@ -244,6 +254,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     for (int s = 0; s < NS; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], TC_CONV);
+    }
+    for (int y = 0; y < NY; ++y) {
+      mbar_init(&y_full[y], 1);
+      mbar_init(&y_empty[y], TC_CONV);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&op_full[b], TC_CONV);
@@ -277,21 +291,22 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // ------------------------------------------------------ TMA producer ----
     if (lane == 0) {
       const uint64_t policy = l2_evict_first_policy();
-      int j = 0, s = 0;
+      int j = 0, s = 0, il = 0;
       uint32_t ph = 0;
       int64_t n = blockIdx.x;
       for (int q = 0; q < total; ++q) {
+        if (j == 0) {  // whole-item Y block
+          const int y = il % NY;
+          if (il >= NY) mbar_wait(&y_empty[y], (uint32_t)(((il / NY) - 1) & 1));
+          const uint32_t yb = (uint32_t)p.T * p.B * 8;
+          mbar_arrive_expect_tx(&y_full[y], yb);
+          bulk_g2s(smem + L.yst + y * L.ybytes, p.Y + (size_t)n * p.T * p.B, yb, &y_full[y], policy);
+        }
         if (q >= NS) mbar_wait(&raw_empty[s], ph ^ 1u);
         const ChunkDesc cd = p.chunks[j];
-        char* st = smem + L.raw + s * stage_bytes;
-        const uint32_t hbytes = (uint32_t)cd.nrows * p.us * 8;
-        const uint32_t ybytes = (uint32_t)cd.nrows * 8;
-        mbar_arrive_expect_tx(&raw_full[s], hbytes + ybytes * p.T);
-        bulk_g2s(st, p.H + ((size_t)n * p.B + cd.row0) * p.us, hbytes, &raw_full[s], policy);
-        float2* ys = reinterpret_cast<float2*>(st) + p.KC * p.us;
-        const float2* ysrc = p.Y + (size_t)n * p.T * p.B + cd.row0;
-        for (int t = 0; t < p.T; ++t)
-          bulk_g2s(ys + t * p.KCP, ysrc + (size_t)t * p.B, ybytes, &raw_full[s], policy);
+        const uint32_t hb = (uint32_t)cd.nrows * p.us * 8;
+        mbar_arrive_expect_tx(&raw_full[s], hb);
+        bulk_g2s(smem + L.hst + s * L.hbytes, p.H + ((size_t)n * p.B + cd.row0) * p.us, hb, &raw_full[s], policy);
         if (++s == NS) {
           s = 0;
           ph ^= 1u;
@@ -299,6 +314,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         if (++j == p.nchunks) {
           j = 0;
           n += gridDim.x;
+          ++il;
         }
       }
     }
@@ -360,16 +376,18 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
       l = x - h;
     };
-    int j = 0, s = 0;
+    int j = 0, s = 0, il = 0;
     uint32_t ph = 0;
     const int ng = HG + p.T;
     for (int q = 0; q < total; ++q) {
       const int b = q & 1;
+      const int y = il % NY;
       mbar_wait(&raw_full[s], ph);
+      mbar_wait(&y_full[y], (uint32_t)((il / NY) & 1));
       if (q >= 2) mbar_wait(&op_empty[b], (uint32_t)(((q >> 1) - 1) & 1));
       const ChunkDesc cd = p.chunks[j];
-      const float* Hf = reinterpret_cast<const float*>(smem + L.raw + s * stage_bytes);
-      const float* Yf = Hf + p.KC * us2;
+      const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
+      const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
       char* hi = smem + L.ops + 2 * b * L.opb;
       char* lo = hi + L.opb;
       const int nr = cd.nrows;
@@ -408,7 +426,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           }
         } else {
           const int t = g - HG;
-          const float* yr = Yf + (t * p.KCP + k0) * 2;  // 4 complex = 2 float4
+          const float* yr = Yf + (t * p.B + k0) * 2;  // 4 complex = 2 float4
           float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
           if (full || k0 + 3 < nr) {
             a0 = *reinterpret_cast<const float4*>(yr);
@@ -452,7 +470,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         s = 0;
         ph ^= 1u;
       }
-      if (++j == p.nchunks) j = 0;
+      if (++j == p.nchunks) {
+        mbar_arrive(&y_empty[y]);  // item's last chunk converted
+        j = 0;
+        ++il;
+      }
     }
   } else if (warp < TC_FIRST_SOLVER) {
     // -------------------------------------------------------- assemblers ----
