@@ -40,6 +40,12 @@ constexpr int TC_CONV = 32 * TC_CONV_W;
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
 
+// byte offset of (feature f, antenna quad qd) in a K=32 operand tile,
+// K-major with the 128-byte swizzle (see umma_desc_sw128)
+__device__ __forceinline__ int sw128_off(int f, int qd) {
+  return (f >> 3) * 1024 + (f & 7) * 128 + ((qd ^ (f & 7)) << 4);
+}
+
 // FD item ring slot: the fusion sums of one item, folded cluster by cluster.
 struct ItemSlotLayout {
   int num, den, harm, wbuf, flags, total;
@@ -338,8 +344,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const uint32_t lo = hi + (uint32_t)L.opb;
         const int nk8 = (cd.nrows + 7) >> 3;
         for (int ks = 0; ks < nk8; ++ks) {
-          const uint64_t ah = umma_desc(hi + ks * 256, 128, 1024);
-          const uint64_t al = umma_desc(lo + ks * 256, 128, 1024);
+          const uint64_t ah = umma_desc_sw128(hi + ks * 32, 1024);
+          const uint64_t al = umma_desc_sw128(lo + ks * 32, 1024);
           umma_tf32(d, ah, ah, idesc, (first && ks == 0) ? 0u : 1u);
           umma_tf32(d, ah, al, idesc, 1u);
           umma_tf32(d, al, ah, idesc, 1u);
@@ -358,8 +364,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   } else if (warp < 2 + TC_CONV_W) {
     // -------------------------------------------------------- converters ----
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
-    // Tile layout: feature f, antenna k -> (f/8)*1024 + (k/4)*128 + (f%8)*16
-    // + (k%4)*4 bytes.  H tasks move a 4-feature x 4-antenna block (4x4
+    // Tile layout (K-major, 128-byte swizzle): feature f, antenna k ->
+    // (f/8)*1024 + (f%8)*128 + ((k/4) ^ (f%8))*16 + (k%4)*4 bytes.  H tasks move a 4-feature x 4-antenna block (4x4
     // transpose in registers), Y tasks one symbol's (re, im) rows x 4 antennas.
     const int ct = tid - 64;
     const int us2 = 2 * p.us;
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const int per_buf = (MB * 8 - MU) * 8;
       const int buf = e / per_buf, r = e % per_buf;
       const int f = MU + r / 8, qd = r % 8;
-      *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + (f >> 3) * 1024 + qd * 128 + (f & 7) * 16) =
+      *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + sw128_off(f, qd)) =
           make_float4(0.f, 0.f, 0.f, 0.f);
     }
     auto split = [](float x, float& h, float& l) {
@@ -420,7 +426,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
             split(cols[c][1], h.y, l.y);
             split(cols[c][2], h.z, l.z);
             split(cols[c][3], h.w, l.w);
-            const int off = (f >> 3) * 1024 + qd * 128 + (f & 7) * 16;
+            const int off = sw128_off(f, qd);
             *reinterpret_cast<float4*>(hi + off) = h;
             *reinterpret_cast<float4*>(lo + off) = l;
           }
@@ -451,14 +457,14 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           split(a0.z, h.y, l.y);
           split(a1.x, h.z, l.z);
           split(a1.z, h.w, l.w);
-          int off = (fr >> 3) * 1024 + qd * 128 + (fr & 7) * 16;
+          int off = sw128_off(fr, qd);
           *reinterpret_cast<float4*>(hi + off) = h;
           *reinterpret_cast<float4*>(lo + off) = l;
           split(a0.y, h.x, l.x);
           split(a0.w, h.y, l.y);
           split(a1.y, h.z, l.z);
           split(a1.w, h.w, l.w);
-          off += 16;  // fr even -> fr + 1 shares the core-matrix block
+          off = sw128_off(fr + 1, qd);
           *reinterpret_cast<float4*>(hi + off) = h;
           *reinterpret_cast<float4*>(lo + off) = l;
         }
