@@ -234,7 +234,14 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
                                                                 int ny) {
   extern __shared__ __align__(1024) char smem[];
   constexpr int N = 2 * UP;
-  constexpr uint32_t TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
+  // independent accumulator chains per unit: hi.hi / hi.lo / lo.hi products
+  // (x2 by k-step parity for U <= 16) accumulate into separate TMEM column
+  // blocks, so consecutive tcgen05.mma do not serialise on one accumulator;
+  // the assembler sums the chains
+  constexpr int NCH = (UP <= 16) ? 6 : 3;
+  constexpr int SW = NCH * N;  // TMEM columns per accumulator slot
+  constexpr uint32_t TMEM_COLS = (2 * SW <= 32) ? 32 : (2 * SW <= 64) ? 64 : (2 * SW <= 128) ? 128
+                                 : (2 * SW <= 256) ? 256 : 512;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
@@ -332,23 +339,31 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const uint32_t ops = smem_u32(smem + L.ops);
       int j = 0, unit = 0;
       bool first = true;
+      bool written[2] = {false, false};  // chain groups (k-step parity) touched in this unit
       for (int q = 0; q < total; ++q) {
         const int b = q & 1;
         mbar_wait(&op_full[b], (uint32_t)((q >> 1) & 1));
         const ChunkDesc cd = p.chunks[j];
         const int a = unit & 1;
-        if (first && unit >= 2) mbar_wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1));
+        if (first) {
+          if (unit >= 2) mbar_wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1));
+          written[0] = written[1] = false;
+        }
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(a * N);
+        const uint32_t dslot = tmem + (uint32_t)(a * SW);
         const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
         const uint32_t lo = hi + (uint32_t)L.opb;
         const int nk8 = (cd.nrows + 7) >> 3;
         for (int ks = 0; ks < nk8; ++ks) {
+          const int grp = (NCH == 6) ? (ks & 1) : 0;
+          const uint32_t acc = written[grp] ? 1u : 0u;
+          written[grp] = true;
+          const uint32_t d = dslot + (uint32_t)(3 * grp * N);
           const uint64_t ah = umma_desc_sw128(hi + ks * 32, 1024);
           const uint64_t al = umma_desc_sw128(lo + ks * 32, 1024);
-          umma_tf32(d, ah, ah, idesc, (first && ks == 0) ? 0u : 1u);
-          umma_tf32(d, ah, al, idesc, 1u);
-          umma_tf32(d, al, ah, idesc, 1u);
+          umma_tf32(d, ah, ah, idesc, acc);
+          umma_tf32(d + N, ah, al, idesc, acc);
+          umma_tf32(d + 2 * N, al, ah, idesc, acc);
         }
         umma_commit(&op_empty[b]);
         const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
@@ -488,12 +503,15 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const int m = 32 * wq + lane;  // accumulator row owned by this thread
     const bool odd = (m & 1) != 0;
     const bool has_rows = 32 * wq < MU;
-    int j = 0, unit = 0;
+    int j = 0, unit = 0, uks = 0;
     for (int q = 0; q < total; ++q) {
       const ChunkDesc cd = p.chunks[j];
       if (++j == p.nchunks) j = 0;
+      uks += (cd.nrows + 7) >> 3;
       const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
       if (!unit_end) continue;
+      const int nch = (NCH == 6 && uks < 2) ? 3 : NCH;  // chain group 1 untouched
+      uks = 0;
       const int sv = unit % nsolv;
       if (unit >= nsolv) mbar_wait(&slot_empty[sv], (uint32_t)(((unit / nsolv) - 1) & 1));
       const int a = unit & 1;
@@ -504,13 +522,19 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         float* Gf = reinterpret_cast<float*>(w.G);
         float* Zf = reinterpret_cast<float*>(w.Z);
         const int LD = w.LD;
-        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * N);
+        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW);
         // 16 accumulator columns = 8 UE columns (re, im) per tcgen05.ld; the
         // partner row (m ^ 1) holds the other component of the same complex row
 #pragma unroll
         for (int h = 0; h < N / 16; ++h) {
           float v[16];
           tmem_ld16(taddr + 16 * h, v);
+          for (int ch = 1; ch < nch; ++ch) {
+            float t16[16];
+            tmem_ld16(taddr + ch * N + 16 * h, t16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += t16[i];
+          }
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
