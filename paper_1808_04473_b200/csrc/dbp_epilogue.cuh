@@ -46,6 +46,7 @@ struct EqParams {
   float* fd_wraw;
   float2 *tr_z, *tr_s, *tr_v;
   float* tr_phi;
+  int ablate;  // debug: 1 skip solver work, 2 skip MMAs, 4 skip conversion (timing studies only)
 };
 
 __device__ __forceinline__ float item_n0(const EqParams& p, int64_t n) {
@@ -84,6 +85,111 @@ struct EpiArgs {
 };
 
 __device__ __forceinline__ void set_status(int* flags, int st) { atomicCAS(flags, 0, st); }
+
+__device__ __forceinline__ float2 shfl2(float2 v, int src) {
+  return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// One-warp ZF / L-MMSE solve (the unit epilogue of the tensor-core kernel's
+// solver warps).  Lane l owns column j = l % UP of the matrix for rows
+// rb + r*RS (rb = l / UP, RS = 32 / UP); the Gauss-Jordan sweep is written
+// branch-free as a rank-1 update  m_ij -= c_i r_j  with
+//   c_i = m_ik (i != k), c_k = p - 1;   r_j = m_kj / p (j != k), r_k = 1 + 1/p
+// (this yields m_kj/p on the pivot row, -m_ik/p on the pivot column and 1/p
+// on the pivot), and the pivot row / column reach the lanes by shuffles, so
+// a step needs neither shared memory nor a barrier.  Padded rows / columns
+// (u < UP) are the identity and stay untouched.
+template <int UP>
+__device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, int lane) {
+  constexpr int RS = 32 / UP;
+  constexpr int EPT = UP * UP / 32;
+  const int u = a.u, T = a.T, LD = w.LD;
+  const int j = lane % UP, rb = lane / UP;
+  float2 m[EPT];
+  float dgl = 1.f;  // original diagonal of the (at most one) diagonal element this lane owns
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = rb + r * RS;
+    float2 v;
+    if (i < u && j < u) {
+      v = w.G[i * LD + j];
+      if (i == j) {
+        v.x += rho;
+        v.y = 0.f;
+        dgl = v.x;
+      }
+    } else {
+      v = make_float2(i == j ? 1.f : 0.f, 0.f);
+    }
+    m[r] = v;
+  }
+  const float tolf = 8.f * (float)u * FLT_EPSILON;
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < UP; ++k) {
+    const int own = (k % RS) * UP + k;  // lane holding (k, k) in register k / RS
+    float p = __shfl_sync(0xffffffffu, m[k / RS].x, own);
+    const float d0 = __shfl_sync(0xffffffffu, dgl, own);
+    if (k < u && !(p > tolf * d0)) {
+      bad = true;
+      p = 1.f;
+    }
+    const float rp = 1.f / p;
+    const float2 rkj = shfl2(m[k / RS], (k % RS) * UP + j);
+    const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      float2 ci = shfl2(m[r], rb * UP + k);
+      if (rb + r * RS == k) ci = make_float2(p - 1.f, 0.f);
+      c_fms(m[r], ci, rj);
+    }
+  }
+  if (bad && lane == 0) set_status(w.flags, ST_SINGULAR);
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    const int i = rb + r * RS;
+    w.G[i * LD + j] = m[r];
+  }
+  __syncwarp();
+  // z = A y_mrc: lane -> UE i = lane % UP, symbols t = rb, rb + RS, ...
+  const bool unb = (a.kind == EQ_LMMSE) && a.unbias;
+  const int i = j;
+  if (i < u) {
+    float2 arow[UP];
+#pragma unroll
+    for (int c = 0; c < UP; c += 2) {
+      const float4 v = *reinterpret_cast<const float4*>(w.G + i * LD + c);
+      arow[c] = make_float2(v.x, v.y);
+      arow[c + 1] = make_float2(v.z, v.w);
+    }
+    const float aii = w.G[i * LD + i].x;
+    const float cgain = 1.f - rho * aii;
+    const float sc = unb ? 1.f / cgain : 1.f;
+    for (int t = rb; t < T; t += RS) {
+      const float2* zr = w.Z + t * LD;
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < UP; c += 2) {
+        if (c < u) {
+          const float4 v = *reinterpret_cast<const float4*>(zr + c);
+          c_fma(acc, arow[c], make_float2(v.x, v.y));
+          if (c + 1 < u) c_fma(acc, arow[c + 1], make_float2(v.z, v.w));
+        }
+      }
+      w.X[t * LD + i] = c_scale(acc, sc);
+    }
+    if (rb == 0) {
+      if (a.kind == EQ_ZF) {
+        w.s2[i] = a.n0 * aii;
+      } else {
+        w.gn[i] = cgain;
+        if (a.unbias && !(cgain > 0.f)) set_status(w.flags, ST_SINGULAR);
+        w.s2[i] = a.unbias ? a.n0 * aii / cgain : a.n0 * aii;
+      }
+    }
+  }
+  __syncwarp();
+}
 
 // ---- linear equalizers on (G, Z) -> X (per symbol), s2, gn --------------
 // equalize.py:130-176 (+ unbiased_output :179-195 when a.unbias).
@@ -125,6 +231,10 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     return;
   }
   const float rho = (a.kind == EQ_LMMSE) ? a.n0 / a.es : 0.f;
+  if constexpr (NT == 32 && UP <= 32) {
+    linear_solve_warp<UP>(w, a, rho, tid);
+    return;
+  }
   // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows
   constexpr int RS = (NT >= UP) ? NT / UP : 1;
   constexpr int EPT = (UP * UP + NT - 1) / NT;

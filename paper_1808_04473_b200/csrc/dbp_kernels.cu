@@ -473,6 +473,7 @@ int dbp_equalize(int arch, int kind, const void* H, const void* Y, int64_t n_ite
   p.iters = iters;
   p.fd_acc = fd_acc;
   p.fd_wraw = fd_wraw;
+  if (const char* ab = getenv("DBP_ABLATE")) p.ablate = atoi(ab);  // timing studies only
   return dispatch_stream(p, static_cast<cudaStream_t>(stream));
 }
 

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   // (x2 by k-step parity for U <= 16) accumulate into separate TMEM column
   // blocks, so consecutive tcgen05.mma do not serialise on one accumulator;
   // the assembler sums the chains
-  constexpr int NCH = (UP <= 16) ? 6 : 3;
+  constexpr int NCH = 1;
   constexpr int SW = NCH * N;  // TMEM columns per accumulator slot
   constexpr uint32_t TMEM_COLS = (2 * SW <= 32) ? 32 : (2 * SW <= 64) ? 64 : (2 * SW <= 128) ? 128
                                  : (2 * SW <= 256) ? 256 : 512;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
         const uint32_t lo = hi + (uint32_t)L.opb;
         const int nk8 = (cd.nrows + 7) >> 3;
-        for (int ks = 0; ks < nk8; ++ks) {
+        for (int ks = 0; ks < ((p.ablate & 2) ? 0 : nk8); ++ks) {
           const int grp = (NCH == 6) ? (ks & 1) : 0;
           const uint32_t acc = written[grp] ? 1u : 0u;
           written[grp] = true;
@@ -385,21 +385,50 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const int ct = tid - 64;
     const int us2 = 2 * p.us;
     constexpr int HG = UP / 2;  // 4-feature groups of the H part
-    // rows between 2(U+T) and MB*8 are zero forever (A padding rows)
-    for (int e = ct; e < 4 * (MB * 8 - MU) * 8; e += TC_CONV) {
-      const int per_buf = (MB * 8 - MU) * 8;
-      const int buf = e / per_buf, r = e % per_buf;
-      const int f = MU + r / 8, qd = r % 8;
-      *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + sw128_off(f, qd)) =
-          make_float4(0.f, 0.f, 0.f, 0.f);
+    // rows between 2(U+T) and MB*8, and H columns past the stored row width
+    // (odd U), are zero forever
+    for (int e = ct; e < 4 * MB * 8 * 8; e += TC_CONV) {
+      const int buf = e / (MB * 64), r = e % (MB * 64);
+      const int f = r / 8, qd = r % 8;
+      if (f >= MU || (f < 2 * UP && f >= us2))
+        *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + sw128_off(f, qd)) =
+            make_float4(0.f, 0.f, 0.f, 0.f);
     }
     auto split = [](float x, float& h, float& l) {
       h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
       l = x - h;
     };
+    // static task list of this thread for a full KC=32-row chunk:
+    // task = (group g, antenna quad qd); g < HG: H features 4g..4g+3,
+    // else symbol t = g - HG (re, im rows)
+    const int ng = HG + p.T;
+    constexpr int MAXT = 2;  // (UP/2 + T) * 8 <= 2 * TC_CONV for UP <= 32, T <= 16
+    int t_ld[MAXT], t_st[MAXT], t_kind[MAXT];
+    int nt_mine = 0;
+#pragma unroll
+    for (int r = 0; r < MAXT; ++r) {
+      const int task = ct + r * TC_CONV;
+      t_kind[r] = -1;
+      t_ld[r] = t_st[r] = 0;
+      if (task < ng * 8) {
+        const int qd = task / ng, g = task - qd * ng;
+        if (g < HG) {
+          if (4 * g < us2) {
+            t_kind[r] = 0;
+            t_ld[r] = 4 * qd * us2 + 4 * g;
+            t_st[r] = (4 * g) * 16 + qd;  // packed: feature base, quad
+          }
+        } else {
+          const int t = g - HG;
+          t_kind[r] = 1;
+          t_ld[r] = (t * p.B + 4 * qd) * 2;
+          t_st[r] = (2 * UP + 2 * t) * 16 + qd;
+        }
+        nt_mine = r + 1;
+      }
+    }
     int j = 0, s = 0, il = 0;
     uint32_t ph = 0;
-    const int ng = HG + p.T;
     for (int q = 0; q < total; ++q) {
       const int b = q & 1;
       const int y = il % NY;
@@ -411,77 +440,124 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
       char* hi = smem + L.ops + 2 * b * L.opb;
       char* lo = hi + L.opb;
-      const int nr = cd.nrows;
-      const int nq = 2 * ((nr + 7) >> 3);  // k-quads incl. zero padding to K % 8
-      const bool full = (nr & 7) == 0;
-      const int ntask = ng * nq;
-      for (int task = ct; task < ntask; task += TC_CONV) {
-        const int qd = task / ng;
-        const int g = task - qd * ng;
-        const int k0 = 4 * qd;
-        if (g < HG) {
-          const int f0 = 4 * g;
-          float4 r[4];
+      if (cd.nrows == 32 && !(p.ablate & 4)) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int k = k0 + i;
-            r[i] = (f0 < us2 && (full || k < nr)) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
-                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          const float c0[4] = {r[0].x, r[1].x, r[2].x, r[3].x};
-          const float c1[4] = {r[0].y, r[1].y, r[2].y, r[3].y};
-          const float c2[4] = {r[0].z, r[1].z, r[2].z, r[3].z};
-          const float c3[4] = {r[0].w, r[1].w, r[2].w, r[3].w};
-          const float* cols[4] = {c0, c1, c2, c3};
+        for (int r = 0; r < MAXT; ++r) {
+          if (r >= nt_mine || t_kind[r] < 0) continue;
+          const int fb = t_st[r] >> 4, qd = t_st[r] & 15;
+          if (t_kind[r] == 0) {
+            const float* src = Hf + t_ld[r];
+            const float4 r0 = *reinterpret_cast<const float4*>(src);
+            const float4 r1 = *reinterpret_cast<const float4*>(src + us2);
+            const float4 r2 = *reinterpret_cast<const float4*>(src + 2 * us2);
+            const float4 r3 = *reinterpret_cast<const float4*>(src + 3 * us2);
+            const float cols[4][4] = {{r0.x, r1.x, r2.x, r3.x}, {r0.y, r1.y, r2.y, r3.y},
+                                      {r0.z, r1.z, r2.z, r3.z}, {r0.w, r1.w, r2.w, r3.w}};
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int f = f0 + c;
+            for (int c = 0; c < 4; ++c) {
+              float4 h, l;
+              split(cols[c][0], h.x, l.x);
+              split(cols[c][1], h.y, l.y);
+              split(cols[c][2], h.z, l.z);
+              split(cols[c][3], h.w, l.w);
+              const int off = sw128_off(fb + c, qd);
+              *reinterpret_cast<float4*>(hi + off) = h;
+              *reinterpret_cast<float4*>(lo + off) = l;
+            }
+          } else {
+            const float* yr = Yf + t_ld[r];
+            const float4 a0 = *reinterpret_cast<const float4*>(yr);
+            const float4 a1 = *reinterpret_cast<const float4*>(yr + 4);
             float4 h, l;
-            split(cols[c][0], h.x, l.x);
-            split(cols[c][1], h.y, l.y);
-            split(cols[c][2], h.z, l.z);
-            split(cols[c][3], h.w, l.w);
-            const int off = sw128_off(f, qd);
+            split(a0.x, h.x, l.x);
+            split(a0.z, h.y, l.y);
+            split(a1.x, h.z, l.z);
+            split(a1.z, h.w, l.w);
+            int off = sw128_off(fb, qd);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+            split(a0.y, h.x, l.x);
+            split(a0.w, h.y, l.y);
+            split(a1.y, h.z, l.z);
+            split(a1.w, h.w, l.w);
+            off = sw128_off(fb + 1, qd);
             *reinterpret_cast<float4*>(hi + off) = h;
             *reinterpret_cast<float4*>(lo + off) = l;
           }
-        } else {
-          const int t = g - HG;
-          const float* yr = Yf + (t * p.B + k0) * 2;  // 4 complex = 2 float4
-          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-          if (full || k0 + 3 < nr) {
-            a0 = *reinterpret_cast<const float4*>(yr);
-            a1 = *reinterpret_cast<const float4*>(yr + 4);
+        }
+      } else {
+        const int nr = cd.nrows;
+        const int nq = 2 * ((nr + 7) >> 3);  // k-quads incl. zero padding to K % 8
+        const bool full = (nr & 7) == 0;
+        const int ntask = (p.ablate & 4) ? 0 : ng * nq;
+        for (int task = ct; task < ntask; task += TC_CONV) {
+          const int qd = task / ng;
+          const int g = task - qd * ng;
+          const int k0 = 4 * qd;
+          if (g < HG) {
+            const int f0 = 4 * g;
+            float4 r[4];
+  #pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int k = k0 + i;
+              r[i] = (f0 < us2 && (full || k < nr)) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float c0[4] = {r[0].x, r[1].x, r[2].x, r[3].x};
+            const float c1[4] = {r[0].y, r[1].y, r[2].y, r[3].y};
+            const float c2[4] = {r[0].z, r[1].z, r[2].z, r[3].z};
+            const float c3[4] = {r[0].w, r[1].w, r[2].w, r[3].w};
+            const float* cols[4] = {c0, c1, c2, c3};
+  #pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int f = f0 + c;
+              float4 h, l;
+              split(cols[c][0], h.x, l.x);
+              split(cols[c][1], h.y, l.y);
+              split(cols[c][2], h.z, l.z);
+              split(cols[c][3], h.w, l.w);
+              const int off = sw128_off(f, qd);
+              *reinterpret_cast<float4*>(hi + off) = h;
+              *reinterpret_cast<float4*>(lo + off) = l;
+            }
           } else {
-            if (k0 < nr) {
-              a0.x = yr[0];
-              a0.y = yr[1];
+            const int t = g - HG;
+            const float* yr = Yf + (t * p.B + k0) * 2;  // 4 complex = 2 float4
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+            if (full || k0 + 3 < nr) {
+              a0 = *reinterpret_cast<const float4*>(yr);
+              a1 = *reinterpret_cast<const float4*>(yr + 4);
+            } else {
+              if (k0 < nr) {
+                a0.x = yr[0];
+                a0.y = yr[1];
+              }
+              if (k0 + 1 < nr) {
+                a0.z = yr[2];
+                a0.w = yr[3];
+              }
+              if (k0 + 2 < nr) {
+                a1.x = yr[4];
+                a1.y = yr[5];
+              }
             }
-            if (k0 + 1 < nr) {
-              a0.z = yr[2];
-              a0.w = yr[3];
-            }
-            if (k0 + 2 < nr) {
-              a1.x = yr[4];
-              a1.y = yr[5];
-            }
+            const int fr = 2 * UP + 2 * t;
+            float4 h, l;
+            split(a0.x, h.x, l.x);
+            split(a0.z, h.y, l.y);
+            split(a1.x, h.z, l.z);
+            split(a1.z, h.w, l.w);
+            int off = sw128_off(fr, qd);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
+            split(a0.y, h.x, l.x);
+            split(a0.w, h.y, l.y);
+            split(a1.y, h.z, l.z);
+            split(a1.w, h.w, l.w);
+            off = sw128_off(fr + 1, qd);
+            *reinterpret_cast<float4*>(hi + off) = h;
+            *reinterpret_cast<float4*>(lo + off) = l;
           }
-          const int fr = 2 * UP + 2 * t;
-          float4 h, l;
-          split(a0.x, h.x, l.x);
-          split(a0.z, h.y, l.y);
-          split(a1.x, h.z, l.z);
-          split(a1.z, h.w, l.w);
-          int off = sw128_off(fr, qd);
-          *reinterpret_cast<float4*>(hi + off) = h;
-          *reinterpret_cast<float4*>(lo + off) = l;
-          split(a0.y, h.x, l.x);
-          split(a0.w, h.y, l.y);
-          split(a1.y, h.z, l.z);
-          split(a1.w, h.w, l.w);
-          off = sw128_off(fr + 1, qd);
-          *reinterpret_cast<float4*>(hi + off) = h;
-          *reinterpret_cast<float4*>(lo + off) = l;
         }
       }
       fence_proxy_async_smem();
@@ -580,7 +656,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       mbar_wait(&slot_full[sv], (uint32_t)(round & 1));
       reset_flags(w, tm);
       tm.sync();
-      if (!fd) {
+      if (p.ablate & 1) {
+      } else if (!fd) {
         unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
       } else {
         const int c = cd.cluster;
