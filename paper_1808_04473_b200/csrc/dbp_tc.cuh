@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           const uint64_t ah = umma_desc_sw128(hi + ks * 32, 1024);
           const uint64_t al = umma_desc_sw128(lo + ks * 32, 1024);
           umma_tf32(d, ah, ah, idesc, acc);
-          umma_tf32(d + N, ah, al, idesc, acc);
-          umma_tf32(d + 2 * N, al, ah, idesc, acc);
+          umma_tf32(NCH >= 3 ? d + N : d, ah, al, idesc, NCH >= 3 ? acc : 1u);
+          umma_tf32(NCH >= 3 ? d + 2 * N : d, al, ah, idesc, NCH >= 3 ? acc : 1u);
         }
         umma_commit(&op_empty[b]);
         const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
