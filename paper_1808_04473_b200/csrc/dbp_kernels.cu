@@ -231,6 +231,10 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     return make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, ns, nyy, p.C, lama, fd, nsv).total <= smem_max;
   };
   int nsolv = TC_MAX_SOLV;
+  // tuning overrides (timing studies only)
+  if (const char* e = getenv("DBP_TC_NS")) p.NS = atoi(e);
+  if (const char* e = getenv("DBP_TC_NY")) ny = atoi(e);
+  if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(1, std::min(TC_MAX_SOLV, atoi(e)));
   while (nsolv > 2 && !fits(p.NS, ny, nsolv)) --nsolv;
   while (p.NS > 3 && !fits(p.NS, ny, nsolv)) --p.NS;
   while (ny > 2 && !fits(p.NS, ny, nsolv)) --ny;

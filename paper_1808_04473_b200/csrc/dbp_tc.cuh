@@ -36,6 +36,7 @@ constexpr int TC_CONV_W = 4;  // converter warps (2..5)
 constexpr int TC_ASM_W = 4;   // assembler warps (6..9)
 constexpr int TC_FIRST_SOLVER = 2 + TC_CONV_W + TC_ASM_W;
 constexpr int TC_MAX_SOLV = 6;
+constexpr int TC_NOP = 4;  // operand tile ring depth (converter -> MMA)
 constexpr int TC_CONV = 32 * TC_CONV_W;
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
@@ -83,7 +84,7 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B,
   const int MB = (2 * UP + 2 * T + 7) / 8;  // 8-row core-matrix blocks used
   int o = 0;
   L.bars = o;
-  o += (2 * NS + 2 * NY + 8 + 2 * TC_MAX_SOLV) * 8;
+  o += (2 * NS + 2 * NY + 2 * TC_NOP + 4 + 2 * TC_MAX_SOLV) * 8;
   L.tmem_slot = o;
   o += 16;
   o = align_up(o, 128);
@@ -96,7 +97,7 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B,
   o = align_up(o, 1024);
   L.ops = o;
   L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
-  o += 4 * L.opb;     // [hi0][lo0][hi1][lo1]
+  o += 2 * TC_NOP * L.opb;  // [hi0][lo0][hi1][lo1]...
   L.work = o;
   L.w = make_work_layout(0, UP, TP, C, lama, false);
   L.work_stride = L.w.total;
@@ -256,8 +257,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   uint64_t* y_full = raw_empty + NS;  // Y item ring
   uint64_t* y_empty = y_full + NY;
   uint64_t* op_full = y_empty + NY;
-  uint64_t* op_empty = op_full + 2;
-  uint64_t* acc_full = op_empty + 2;
+  uint64_t* op_empty = op_full + TC_NOP;
+  uint64_t* acc_full = op_empty + TC_NOP;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* slot_full = acc_empty + 2;
   uint64_t* slot_empty = slot_full + TC_MAX_SOLV;
@@ -272,9 +273,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       mbar_init(&y_full[y], 1);
       mbar_init(&y_empty[y], TC_CONV);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < TC_NOP; ++b) {
       mbar_init(&op_full[b], TC_CONV);
       mbar_init(&op_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], TC_ASM);
     }
@@ -341,8 +344,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       bool first = true;
       bool written[2] = {false, false};  // chain groups (k-step parity) touched in this unit
       for (int q = 0; q < total; ++q) {
-        const int b = q & 1;
-        mbar_wait(&op_full[b], (uint32_t)((q >> 1) & 1));
+        const int b = q % TC_NOP;
+        mbar_wait(&op_full[b], (uint32_t)((q / TC_NOP) & 1));
         const ChunkDesc cd = p.chunks[j];
         const int a = unit & 1;
         if (first) {
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     constexpr int HG = UP / 2;  // 4-feature groups of the H part
     // rows between 2(U+T) and MB*8, and H columns past the stored row width
     // (odd U), are zero forever
-    for (int e = ct; e < 4 * MB * 8 * 8; e += TC_CONV) {
+    for (int e = ct; e < 2 * TC_NOP * MB * 8 * 8; e += TC_CONV) {
       const int buf = e / (MB * 64), r = e % (MB * 64);
       const int f = r / 8, qd = r % 8;
       if (f >= MU || (f < 2 * UP && f >= us2))
@@ -430,11 +433,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     int j = 0, s = 0, il = 0;
     uint32_t ph = 0;
     for (int q = 0; q < total; ++q) {
-      const int b = q & 1;
+      const int b = q % TC_NOP;
       const int y = il % NY;
       mbar_wait(&raw_full[s], ph);
       mbar_wait(&y_full[y], (uint32_t)((il / NY) & 1));
-      if (q >= 2) mbar_wait(&op_empty[b], (uint32_t)(((q >> 1) - 1) & 1));
+      if (q >= TC_NOP) mbar_wait(&op_empty[b], (uint32_t)(((q / TC_NOP) - 1) & 1));
       const ChunkDesc cd = p.chunks[j];
       const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
       const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
