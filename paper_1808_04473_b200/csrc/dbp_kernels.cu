@@ -246,7 +246,24 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
   const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count());
+  static long long* dbg = nullptr;
+  const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
+  if (debug) {
+    if (!dbg) cudaMalloc(&dbg, 20 * sizeof(long long));
+    cudaMemsetAsync(dbg, 0, 20 * sizeof(long long), st);
+    p.dbg = dbg;
+  }
   kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv, ny);
+  if (debug) {
+    long long h[20];
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    static const char* names[5] = {"producer", "mma", "converter", "assembler", "solver"};
+    fprintf(stderr, "[dbp tc debug] NS=%d NY=%d nsolv=%d (cycles summed over CTAs, one lane per role)\n", p.NS, ny,
+            nsolv);
+    for (int r = 0; r < 5; ++r)
+      fprintf(stderr, "  %-9s total %.3e  wait1 %.3e  wait2 %.3e  wait3 %.3e\n", names[r], (double)h[r * 4],
+              (double)h[r * 4 + 1], (double)h[r * 4 + 2], (double)h[r * 4 + 3]);
+  }
   return cuda_check("tc_kernel");
 }
 

@@ -230,6 +230,21 @@ __device__ void fd_fold(const Work& w, char* slot, const ItemSlotLayout& S, cons
   if (tm.t == 0) *turn = (c == C - 1) ? (il + nir) * C : key + 1;
 }
 
+// Debug instrumentation (p.dbg != nullptr, set by DBP_TC_DEBUG): per-CTA
+// cycle counters of each role's waits, for pipeline studies.
+struct WaitClock {
+  long long* acc;  // nullptr when disabled
+  __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int slot) {
+    if (!acc) {
+      mbar_wait(bar, parity);
+      return;
+    }
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc[slot] += clock64() - t0;
+  }
+};
+
 template <int UP>
 __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv,
                                                                 int ny) {
@@ -302,6 +317,12 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const int64_t my_items = (p.n_items > blockIdx.x) ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int total = (int)(my_items * p.nchunks);
   const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
+  // role id for the debug counters: 0 producer, 1 mma, 2 converter, 3 assembler, 4 solver
+  const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp < 2 + TC_CONV_W ? 2 : warp < TC_FIRST_SOLVER ? 3 : 4;
+  const bool rec = p.dbg && lane == 0 && (warp < 3 || warp == 2 + TC_CONV_W || warp == TC_FIRST_SOLVER);
+  long long cnt[4] = {0, 0, 0, 0};
+  WaitClock wc{rec ? cnt : nullptr};
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ----
@@ -313,12 +334,12 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       for (int q = 0; q < total; ++q) {
         if (j == 0) {  // whole-item Y block
           const int y = il % NY;
-          if (il >= NY) mbar_wait(&y_empty[y], (uint32_t)(((il / NY) - 1) & 1));
+          if (il >= NY) wc.wait(&y_empty[y], (uint32_t)(((il / NY) - 1) & 1), 1);
           const uint32_t yb = (uint32_t)p.T * p.B * 8;
           mbar_arrive_expect_tx(&y_full[y], yb);
           bulk_g2s(smem + L.yst + y * L.ybytes, p.Y + (size_t)n * p.T * p.B, yb, &y_full[y], policy);
         }
-        if (q >= NS) mbar_wait(&raw_empty[s], ph ^ 1u);
+        if (q >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
         const ChunkDesc cd = p.chunks[j];
         const uint32_t hb = (uint32_t)cd.nrows * p.us * 8;
         mbar_arrive_expect_tx(&raw_full[s], hb);
@@ -345,11 +366,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       bool written[2] = {false, false};  // chain groups (k-step parity) touched in this unit
       for (int q = 0; q < total; ++q) {
         const int b = q % TC_NOP;
-        mbar_wait(&op_full[b], (uint32_t)((q / TC_NOP) & 1));
+        wc.wait(&op_full[b], (uint32_t)((q / TC_NOP) & 1), 1);
         const ChunkDesc cd = p.chunks[j];
         const int a = unit & 1;
         if (first) {
-          if (unit >= 2) mbar_wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1));
+          if (unit >= 2) wc.wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1), 2);
           written[0] = written[1] = false;
         }
         tc_fence_after();
@@ -435,9 +456,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     for (int q = 0; q < total; ++q) {
       const int b = q % TC_NOP;
       const int y = il % NY;
-      mbar_wait(&raw_full[s], ph);
-      mbar_wait(&y_full[y], (uint32_t)((il / NY) & 1));
-      if (q >= TC_NOP) mbar_wait(&op_empty[b], (uint32_t)(((q / TC_NOP) - 1) & 1));
+      wc.wait(&raw_full[s], ph, 1);
+      wc.wait(&y_full[y], (uint32_t)((il / NY) & 1), 2);
+      if (q >= TC_NOP) wc.wait(&op_empty[b], (uint32_t)(((q / TC_NOP) - 1) & 1), 3);
       const ChunkDesc cd = p.chunks[j];
       const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
       const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
@@ -592,9 +613,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const int nch = (NCH == 6 && uks < 2) ? 3 : NCH;  // chain group 1 untouched
       uks = 0;
       const int sv = unit % nsolv;
-      if (unit >= nsolv) mbar_wait(&slot_empty[sv], (uint32_t)(((unit / nsolv) - 1) & 1));
+      if (unit >= nsolv) wc.wait(&slot_empty[sv], (uint32_t)(((unit / nsolv) - 1) & 1), 1);
       const int a = unit & 1;
-      mbar_wait(&acc_full[a], (uint32_t)((unit >> 1) & 1));
+      wc.wait(&acc_full[a], (uint32_t)((unit >> 1) & 1), 2);
       tc_fence_after();
       if (has_rows) {
         const Work w = work_at(smem, L, sv, UP);
@@ -656,7 +677,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const int round = unit / nsolv;
       ++unit;
       if (!my) continue;
-      mbar_wait(&slot_full[sv], (uint32_t)(round & 1));
+      wc.wait(&slot_full[sv], (uint32_t)(round & 1), 1);
       reset_flags(w, tm);
       tm.sync();
       if (p.ablate & 1) {
@@ -685,6 +706,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       tm.sync();
       if (lane == 0) mbar_arrive(&slot_empty[sv]);
     }
+  }
+  if (rec) {
+    cnt[0] = clock64() - t_start;
+    for (int k = 0; k < 4; ++k) atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg + role * 4 + k),
+                                          (unsigned long long)cnt[k]);
   }
   tc_fence_before();
   __syncthreads();
