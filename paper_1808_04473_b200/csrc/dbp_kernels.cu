@@ -222,24 +222,36 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // two units per operand tile / MMA when both fit in M = 128 rows and every
+  // unit has the same chunk structure (uniform clusters for per-cluster units)
+  const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
+  bool uniform = true;
+  const int upi = per_cluster ? p.C : 1;
+  if (p.nchunks % upi) uniform = false;
+  const int cpu = uniform ? p.nchunks / upi : 0;
+  for (int c = 1; uniform && c < upi; ++c)
+    for (int j = 0; j < cpu; ++j)
+      if (p.chunks[c * cpu + j].nrows != p.chunks[j].nrows || p.chunks[c * cpu + j].cluster != c) uniform = false;
+  if (!uniform) return 1;  // ragged clusters: SIMT kernel
+  p.pair = (2 * (2 * UP + 2 * p.T) <= 128) ? 2 : 1;
+  if (const char* e = getenv("DBP_TC_PAIR")) p.pair = std::max(1, std::min(2, atoi(e)));
   // staging depth for ~64 KB of HBM reads in flight per SM (Little's law at
   // ~1.5 us latency), then as many solver warps as shared memory allows
   const int ybytes = p.T * p.B * 8;
-  int ny = ybytes <= 16384 ? 3 : 2;
+  int ny = p.pair == 2 ? 4 : (ybytes <= 16384 ? 3 : 2);
   p.NS = std::max(4, std::min(12, (64 * 1024 - ny * ybytes) / (p.KC * p.us * 8)));
   auto fits = [&](int ns, int nyy, int nsv) {
-    return make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, ns, nyy, p.C, lama, fd, nsv).total <= smem_max;
+    return make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, ns, nyy, p.C, lama, fd, nsv, p.pair).total <= smem_max;
   };
   int nsolv = TC_MAX_SOLV;
   // tuning overrides (timing studies only)
   if (const char* e = getenv("DBP_TC_NS")) p.NS = atoi(e);
   if (const char* e = getenv("DBP_TC_NY")) ny = atoi(e);
-  if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(1, std::min(TC_MAX_SOLV, atoi(e)));
+  if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(2, std::min(TC_MAX_SOLV, atoi(e)));
   while (nsolv > 2 && !fits(p.NS, ny, nsolv)) --nsolv;
   while (p.NS > 3 && !fits(p.NS, ny, nsolv)) --p.NS;
   while (ny > 2 && !fits(p.NS, ny, nsolv)) --ny;
-  while (nsolv > 1 && !fits(p.NS, ny, nsolv)) --nsolv;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, p.NS, ny, p.C, lama, fd, nsolv);
+  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, p.NS, ny, p.C, lama, fd, nsolv, p.pair);
   if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
   auto kern = tc_kernel<UP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)

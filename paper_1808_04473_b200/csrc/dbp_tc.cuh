@@ -79,9 +79,9 @@ struct TcLayout {
 // and a ring of NY whole-item Y blocks (T x B, one bulk copy per item -- the
 // per-symbol rows of a chunk are only 8*KC bytes and would cost T tiny copies).
 __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B, int us, int KC, int NS, int NY,
-                                                   int C, bool lama, bool fd, int nsolv) {
+                                                   int C, bool lama, bool fd, int nsolv, int pair) {
   TcLayout L;
-  const int MB = (2 * UP + 2 * T + 7) / 8;  // 8-row core-matrix blocks used
+  const int MB = (pair * (2 * UP + 2 * T) + 7) / 8;  // 8-row core-matrix blocks used
   int o = 0;
   L.bars = o;
   o += (2 * NS + 2 * NY + 2 * TC_NOP + 4 + 2 * TC_MAX_SOLV) * 8;
@@ -245,17 +245,39 @@ struct WaitClock {
   }
 };
 
+// Stream order.  A CTA owns U_tot units (items for PD / STATS-summed, clusters
+// for FD / STATS-per-cluster), unit u = (CTA-local item u / upi, cluster
+// u % upi).  With pair == 2 two units share every operand tile (rows
+// [h*2UP, (h+1)*2UP) = H features of half h, rows 2*2UP + h*2T.. = its Y
+// features) and every tcgen05.mma (N = 2 * 2UP): the fixed ~46-cycle cost of
+// one small tf32 MMA is paid once for two units.  Stream position q walks
+// pairs v, then chunk j < cpu of a unit, then half h < pair.
+struct Stream {
+  int pair, cpu, upi, U_tot;
+  int v, j, h;  // current position
+  __device__ __forceinline__ void advance() {
+    if (++h == pair) {
+      h = 0;
+      if (++j == cpu) {
+        j = 0;
+        ++v;
+      }
+    }
+  }
+  __device__ __forceinline__ int unit() const { return v * pair + h; }
+  __device__ __forceinline__ bool null() const { return unit() >= U_tot; }
+  __device__ __forceinline__ int item() const { return unit() / upi; }
+  __device__ __forceinline__ int cluster() const { return unit() % upi; }
+  __device__ __forceinline__ int chunk_index() const { return cluster() * cpu + j; }
+};
+
 template <int UP>
 __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv,
                                                                 int ny) {
   extern __shared__ __align__(1024) char smem[];
-  constexpr int N = 2 * UP;
-  // independent accumulator chains per unit: hi.hi / hi.lo / lo.hi products
-  // (x2 by k-step parity for U <= 16) accumulate into separate TMEM column
-  // blocks, so consecutive tcgen05.mma do not serialise on one accumulator;
-  // the assembler sums the chains
-  constexpr int NCH = 1;
-  constexpr int SW = NCH * N;  // TMEM columns per accumulator slot
+  const int pair = p.pair;
+  const int N = pair * 2 * UP;  // MMA N: the H features of both halves
+  constexpr int SW = 2 * 2 * UP;  // TMEM columns per accumulator slot (room for pair == 2)
   constexpr uint32_t TMEM_COLS = (2 * SW <= 32) ? 32 : (2 * SW <= 64) ? 64 : (2 * SW <= 128) ? 128
                                  : (2 * SW <= 256) ? 256 : 512;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -263,9 +285,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   const int NS = p.NS;
   const int NY = ny;
-  const int MU = 2 * UP + 2 * p.T;
+  const int T = p.T;
+  const int YB = pair * 2 * UP;          // first Y row of the tile
+  const int MU = YB + pair * 2 * T;      // rows in use
   const int MB = (MU + 7) / 8;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, NS, NY, p.C, lama, fd, nsolv);
+  const TcLayout L = make_tc_layout(UP, p.TP, T, p.B, p.us, p.KC, NS, NY, p.C, lama, fd, nsolv, pair);
   const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // H chunk ring
   uint64_t* raw_empty = raw_full + NS;
@@ -289,7 +313,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       mbar_init(&y_empty[y], TC_CONV);
     }
     for (int b = 0; b < TC_NOP; ++b) {
-      mbar_init(&op_full[b], TC_CONV);
+      mbar_init(&op_full[b], TC_CONV * pair);
       mbar_init(&op_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -315,8 +339,13 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const uint32_t tmem = *tmem_slot;
 
   const int64_t my_items = (p.n_items > blockIdx.x) ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int total = (int)(my_items * p.nchunks);
   const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
+  const int upi = per_cluster ? p.C : 1;
+  const int cpu = p.nchunks / upi;
+  const int U_tot = (int)my_items * upi;
+  const int n_pairs = (U_tot + pair - 1) / pair;
+  const int S_tot = n_pairs * pair * cpu;  // stream length
+  const Stream s0{pair, cpu, upi, U_tot, 0, 0, 0};
   // role id for the debug counters: 0 producer, 1 mma, 2 converter, 3 assembler, 4 solver
   const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp < 2 + TC_CONV_W ? 2 : warp < TC_FIRST_SOLVER ? 3 : 4;
   const bool rec = p.dbg && lane == 0 && (warp < 3 || warp == 2 + TC_CONV_W || warp == TC_FIRST_SOLVER);
@@ -328,30 +357,33 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // ------------------------------------------------------ TMA producer ----
     if (lane == 0) {
       const uint64_t policy = l2_evict_first_policy();
-      int j = 0, s = 0, il = 0;
+      Stream st = s0;
+      int s = 0;
       uint32_t ph = 0;
-      int64_t n = blockIdx.x;
-      for (int q = 0; q < total; ++q) {
-        if (j == 0) {  // whole-item Y block
+      for (int q = 0; q < S_tot; ++q, st.advance()) {
+        const bool nul = st.null();
+        const int il = st.item();
+        const int64_t n = blockIdx.x + (int64_t)il * gridDim.x;
+        if (!nul && st.cluster() == 0 && st.j == 0) {  // whole-item Y block
           const int y = il % NY;
           if (il >= NY) wc.wait(&y_empty[y], (uint32_t)(((il / NY) - 1) & 1), 1);
-          const uint32_t yb = (uint32_t)p.T * p.B * 8;
+          const uint32_t yb = (uint32_t)T * p.B * 8;
           mbar_arrive_expect_tx(&y_full[y], yb);
-          bulk_g2s(smem + L.yst + y * L.ybytes, p.Y + (size_t)n * p.T * p.B, yb, &y_full[y], policy);
+          bulk_g2s(smem + L.yst + y * L.ybytes, p.Y + (size_t)n * T * p.B, yb, &y_full[y], policy);
         }
         if (q >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
-        const ChunkDesc cd = p.chunks[j];
-        const uint32_t hb = (uint32_t)cd.nrows * p.us * 8;
-        mbar_arrive_expect_tx(&raw_full[s], hb);
-        bulk_g2s(smem + L.hst + s * L.hbytes, p.H + ((size_t)n * p.B + cd.row0) * p.us, hb, &raw_full[s], policy);
+        if (nul) {
+          mbar_arrive(&raw_full[s]);  // empty chunk: the converter writes zeros
+        } else {
+          const ChunkDesc cd = p.chunks[st.chunk_index()];
+          const uint32_t hb = (uint32_t)cd.nrows * p.us * 8;
+          mbar_arrive_expect_tx(&raw_full[s], hb);
+          bulk_g2s(smem + L.hst + s * L.hbytes, p.H + ((size_t)n * p.B + cd.row0) * p.us, hb, &raw_full[s],
+                   policy);
+        }
         if (++s == NS) {
           s = 0;
           ph ^= 1u;
-        }
-        if (++j == p.nchunks) {
-          j = 0;
-          n += gridDim.x;
-          ++il;
         }
       }
     }
@@ -361,60 +393,52 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_tf32(128, N);
       const uint32_t ops = smem_u32(smem + L.ops);
-      int j = 0, unit = 0;
-      bool first = true;
-      bool written[2] = {false, false};  // chain groups (k-step parity) touched in this unit
-      for (int q = 0; q < total; ++q) {
-        const int b = q % TC_NOP;
-        wc.wait(&op_full[b], (uint32_t)((q / TC_NOP) & 1), 1);
-        const ChunkDesc cd = p.chunks[j];
-        const int a = unit & 1;
-        if (first) {
-          if (unit >= 2) wc.wait(&acc_empty[a], (uint32_t)(((unit >> 1) - 1) & 1), 2);
-          written[0] = written[1] = false;
-        }
+      Stream st = s0;
+      for (int pq = 0; pq < S_tot / pair; ++pq) {  // one tile per (pair v, chunk j)
+        const int b = pq % TC_NOP;
+        const int v = pq / cpu, j = pq - v * cpu;
+        wc.wait(&op_full[b], (uint32_t)((pq / TC_NOP) & 1), 1);
+        st.v = v;
+        st.j = j;
+        st.h = 0;
+        const ChunkDesc cd = p.chunks[st.chunk_index()];
+        const int a = v & 1;
+        if (j == 0 && v >= 2) wc.wait(&acc_empty[a], (uint32_t)(((v >> 1) - 1) & 1), 2);
         tc_fence_after();
-        const uint32_t dslot = tmem + (uint32_t)(a * SW);
+        const uint32_t d = tmem + (uint32_t)(a * SW);
         const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
         const uint32_t lo = hi + (uint32_t)L.opb;
-        const int nk8 = (cd.nrows + 7) >> 3;
-        for (int ks = 0; ks < ((p.ablate & 2) ? 0 : nk8); ++ks) {
-          const int grp = (NCH == 6) ? (ks & 1) : 0;
-          const uint32_t acc = written[grp] ? 1u : 0u;
-          written[grp] = true;
-          const uint32_t d = dslot + (uint32_t)(3 * grp * N);
+        const int nk8 = (p.ablate & 2) ? 0 : (cd.nrows + 7) >> 3;
+        for (int ks = 0; ks < nk8; ++ks) {
+          const uint32_t acc = (j == 0 && ks == 0) ? 0u : 1u;
           const uint64_t ah = umma_desc_sw128(hi + ks * 32, 1024);
           const uint64_t al = umma_desc_sw128(lo + ks * 32, 1024);
           umma_tf32(d, ah, ah, idesc, acc);
-          umma_tf32(NCH >= 3 ? d + N : d, ah, al, idesc, NCH >= 3 ? acc : 1u);
-          umma_tf32(NCH >= 3 ? d + 2 * N : d, al, ah, idesc, NCH >= 3 ? acc : 1u);
+          umma_tf32(d, ah, al, idesc, 1u);
+          umma_tf32(d, al, ah, idesc, 1u);
         }
         umma_commit(&op_empty[b]);
-        const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
-        if (unit_end) {
-          umma_commit(&acc_full[a]);
-          ++unit;
-        }
-        first = unit_end;
-        if (++j == p.nchunks) j = 0;
+        if (j == cpu - 1) umma_commit(&acc_full[a]);
       }
     }
     __syncwarp();
   } else if (warp < 2 + TC_CONV_W) {
     // -------------------------------------------------------- converters ----
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
-    // Tile layout (K-major, 128-byte swizzle): feature f, antenna k ->
-    // (f/8)*1024 + (f%8)*128 + ((k/4) ^ (f%8))*16 + (k%4)*4 bytes.  H tasks move a 4-feature x 4-antenna block (4x4
-    // transpose in registers), Y tasks one symbol's (re, im) rows x 4 antennas.
+    // Tile layout (K-major, 128-byte swizzle): row f, antenna k ->
+    // (f/8)*1024 + (f%8)*128 + ((k/4) ^ (f%8))*16 + (k%4)*4 bytes.  H tasks move
+    // a 4-feature x 4-antenna block (4x4 transpose in registers), Y tasks one
+    // symbol's (re, im) rows x 4 antennas.
     const int ct = tid - 64;
     const int us2 = 2 * p.us;
-    constexpr int HG = UP / 2;  // 4-feature groups of the H part
-    // rows between 2(U+T) and MB*8, and H columns past the stored row width
+    constexpr int HG = UP / 2;  // 4-feature groups of the H part of one half
+    // rows past the ones in use, and H columns past the stored row width
     // (odd U), are zero forever
     for (int e = ct; e < 2 * TC_NOP * MB * 8 * 8; e += TC_CONV) {
       const int buf = e / (MB * 64), r = e % (MB * 64);
       const int f = r / 8, qd = r % 8;
-      if (f >= MU || (f < 2 * UP && f >= us2))
+      const bool hpad = f < YB && (f % (2 * UP)) >= us2;
+      if (f >= MU || hpad)
         *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + sw128_off(f, qd)) =
             make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -422,53 +446,74 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
       l = x - h;
     };
-    // static task list of this thread for a full KC=32-row chunk:
-    // task = (group g, antenna quad qd); g < HG: H features 4g..4g+3,
-    // else symbol t = g - HG (re, im rows)
-    const int ng = HG + p.T;
+    // static task list of this thread for a full KC=32-row chunk of one half:
+    // task = (group g, antenna quad qd); g < HG: H features 4g..4g+3, else
+    // symbol t = g - HG (re, im rows); store offsets for half 0 (half 1 adds
+    // the row shift, which keeps the swizzle phase: shifts are multiples of 8)
+    const int ng = HG + T;
     constexpr int MAXT = 2;  // (UP/2 + T) * 8 <= 2 * TC_CONV for UP <= 32, T <= 16
-    int t_ld[MAXT], t_st[MAXT], t_kind[MAXT];
-    int nt_mine = 0;
+    int t_ld[MAXT], t_kind[MAXT], t_st[MAXT][4];
 #pragma unroll
     for (int r = 0; r < MAXT; ++r) {
       const int task = ct + r * TC_CONV;
       t_kind[r] = -1;
-      t_ld[r] = t_st[r] = 0;
+      t_ld[r] = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) t_st[r][c] = 0;
       if (task < ng * 8) {
         const int qd = task / ng, g = task - qd * ng;
         if (g < HG) {
           if (4 * g < us2) {
             t_kind[r] = 0;
             t_ld[r] = 4 * qd * us2 + 4 * g;
-            t_st[r] = (4 * g) * 16 + qd;  // packed: feature base, quad
+#pragma unroll
+            for (int c = 0; c < 4; ++c) t_st[r][c] = sw128_off(4 * g + c, qd);
           }
         } else {
           const int t = g - HG;
           t_kind[r] = 1;
           t_ld[r] = (t * p.B + 4 * qd) * 2;
-          t_st[r] = (2 * UP + 2 * t) * 16 + qd;
+          // (re, im) rows of symbol t for half 0 and half 1 (a 2T-row shift
+          // need not preserve the swizzle phase, so both are precomputed)
+          t_st[r][0] = sw128_off(YB + 2 * t, qd);
+          t_st[r][1] = sw128_off(YB + 2 * t + 1, qd);
+          t_st[r][2] = sw128_off(YB + 2 * T + 2 * t, qd);
+          t_st[r][3] = sw128_off(YB + 2 * T + 2 * t + 1, qd);
         }
-        nt_mine = r + 1;
       }
     }
-    int j = 0, s = 0, il = 0;
+    Stream st = s0;
+    int s = 0;
     uint32_t ph = 0;
-    for (int q = 0; q < total; ++q) {
-      const int b = q % TC_NOP;
+    for (int q = 0; q < S_tot; ++q, st.advance()) {
+      const int pq = q / pair;
+      const int b = pq % TC_NOP;
+      const int h = st.h;
+      const bool nul = st.null();
+      const int il = st.item();
       const int y = il % NY;
       wc.wait(&raw_full[s], ph, 1);
-      wc.wait(&y_full[y], (uint32_t)((il / NY) & 1), 2);
-      if (q >= TC_NOP) wc.wait(&op_empty[b], (uint32_t)(((q / TC_NOP) - 1) & 1), 3);
-      const ChunkDesc cd = p.chunks[j];
+      if (!nul) wc.wait(&y_full[y], (uint32_t)((il / NY) & 1), 2);
+      if (h == 0 && pq >= TC_NOP) wc.wait(&op_empty[b], (uint32_t)(((pq / TC_NOP) - 1) & 1), 3);
+      const ChunkDesc cd = p.chunks[st.chunk_index()];
       const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
       const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
       char* hi = smem + L.ops + 2 * b * L.opb;
       char* lo = hi + L.opb;
-      if (cd.nrows == 32 && !(p.ablate & 4)) {
+      // half h: H rows shift by h*2UP (a multiple of 8 rows: same swizzle
+      // phase); Y rows use the per-half precomputed offsets
+      const int hshift = h * 2 * UP * 128;
+      if (nul) {
+        for (int e = ct; e < (2 * UP + 2 * T) * 8; e += TC_CONV) {
+          const int r = e / 8, qd = e % 8;
+          const int f = (r < 2 * UP) ? h * 2 * UP + r : YB + h * 2 * T + (r - 2 * UP);
+          *reinterpret_cast<float4*>(hi + sw128_off(f, qd)) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(lo + sw128_off(f, qd)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else if (cd.nrows == 32 && !(p.ablate & 4)) {
 #pragma unroll
         for (int r = 0; r < MAXT; ++r) {
-          if (r >= nt_mine || t_kind[r] < 0) continue;
-          const int fb = t_st[r] >> 4, qd = t_st[r] & 15;
+          if (t_kind[r] < 0) continue;
           if (t_kind[r] == 0) {
             const float* src = Hf + t_ld[r];
             const float4 r0 = *reinterpret_cast<const float4*>(src);
@@ -479,40 +524,40 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
                                       {r0.z, r1.z, r2.z, r3.z}, {r0.w, r1.w, r2.w, r3.w}};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              float4 h, l;
-              split(cols[c][0], h.x, l.x);
-              split(cols[c][1], h.y, l.y);
-              split(cols[c][2], h.z, l.z);
-              split(cols[c][3], h.w, l.w);
-              const int off = sw128_off(fb + c, qd);
-              *reinterpret_cast<float4*>(hi + off) = h;
-              *reinterpret_cast<float4*>(lo + off) = l;
+              float4 hh, ll;
+              split(cols[c][0], hh.x, ll.x);
+              split(cols[c][1], hh.y, ll.y);
+              split(cols[c][2], hh.z, ll.z);
+              split(cols[c][3], hh.w, ll.w);
+              const int off = t_st[r][c] + hshift;
+              *reinterpret_cast<float4*>(hi + off) = hh;
+              *reinterpret_cast<float4*>(lo + off) = ll;
             }
           } else {
             const float* yr = Yf + t_ld[r];
             const float4 a0 = *reinterpret_cast<const float4*>(yr);
             const float4 a1 = *reinterpret_cast<const float4*>(yr + 4);
-            float4 h, l;
-            split(a0.x, h.x, l.x);
-            split(a0.z, h.y, l.y);
-            split(a1.x, h.z, l.z);
-            split(a1.z, h.w, l.w);
-            int off = sw128_off(fb, qd);
-            *reinterpret_cast<float4*>(hi + off) = h;
-            *reinterpret_cast<float4*>(lo + off) = l;
-            split(a0.y, h.x, l.x);
-            split(a0.w, h.y, l.y);
-            split(a1.y, h.z, l.z);
-            split(a1.w, h.w, l.w);
-            off = sw128_off(fb + 1, qd);
-            *reinterpret_cast<float4*>(hi + off) = h;
-            *reinterpret_cast<float4*>(lo + off) = l;
+            float4 hh, ll;
+            split(a0.x, hh.x, ll.x);
+            split(a0.z, hh.y, ll.y);
+            split(a1.x, hh.z, ll.z);
+            split(a1.z, hh.w, ll.w);
+            const int o_re = h ? t_st[r][2] : t_st[r][0];
+            const int o_im = h ? t_st[r][3] : t_st[r][1];
+            *reinterpret_cast<float4*>(hi + o_re) = hh;
+            *reinterpret_cast<float4*>(lo + o_re) = ll;
+            split(a0.y, hh.x, ll.x);
+            split(a0.w, hh.y, ll.y);
+            split(a1.y, hh.z, ll.z);
+            split(a1.w, hh.w, ll.w);
+            *reinterpret_cast<float4*>(hi + o_im) = hh;
+            *reinterpret_cast<float4*>(lo + o_im) = ll;
           }
         }
       } else {
+        // generic chunk (fewer rows, or rows not a multiple of 8): zero-pad K
         const int nr = cd.nrows;
-        const int nq = 2 * ((nr + 7) >> 3);  // k-quads incl. zero padding to K % 8
-        const bool full = (nr & 7) == 0;
+        const int nq = 2 * ((nr + 7) >> 3);
         const int ntask = (p.ablate & 4) ? 0 : ng * nq;
         for (int task = ct; task < ntask; task += TC_CONV) {
           const int qd = task / ng;
@@ -520,67 +565,60 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           const int k0 = 4 * qd;
           if (g < HG) {
             const int f0 = 4 * g;
-            float4 r[4];
-  #pragma unroll
+            float4 r4[4];
+#pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int k = k0 + i;
-              r[i] = (f0 < us2 && (full || k < nr)) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+              r4[i] = (f0 < us2 && k < nr) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            const float c0[4] = {r[0].x, r[1].x, r[2].x, r[3].x};
-            const float c1[4] = {r[0].y, r[1].y, r[2].y, r[3].y};
-            const float c2[4] = {r[0].z, r[1].z, r[2].z, r[3].z};
-            const float c3[4] = {r[0].w, r[1].w, r[2].w, r[3].w};
-            const float* cols[4] = {c0, c1, c2, c3};
-  #pragma unroll
+            const float cols[4][4] = {{r4[0].x, r4[1].x, r4[2].x, r4[3].x}, {r4[0].y, r4[1].y, r4[2].y, r4[3].y},
+                                      {r4[0].z, r4[1].z, r4[2].z, r4[3].z}, {r4[0].w, r4[1].w, r4[2].w, r4[3].w}};
+#pragma unroll
             for (int c = 0; c < 4; ++c) {
-              const int f = f0 + c;
-              float4 h, l;
-              split(cols[c][0], h.x, l.x);
-              split(cols[c][1], h.y, l.y);
-              split(cols[c][2], h.z, l.z);
-              split(cols[c][3], h.w, l.w);
-              const int off = sw128_off(f, qd);
-              *reinterpret_cast<float4*>(hi + off) = h;
-              *reinterpret_cast<float4*>(lo + off) = l;
+              float4 hh, ll;
+              split(cols[c][0], hh.x, ll.x);
+              split(cols[c][1], hh.y, ll.y);
+              split(cols[c][2], hh.z, ll.z);
+              split(cols[c][3], hh.w, ll.w);
+              const int off = sw128_off(h * 2 * UP + f0 + c, qd);
+              *reinterpret_cast<float4*>(hi + off) = hh;
+              *reinterpret_cast<float4*>(lo + off) = ll;
             }
           } else {
             const int t = g - HG;
-            const float* yr = Yf + (t * p.B + k0) * 2;  // 4 complex = 2 float4
+            const float* yr = Yf + (t * p.B + k0) * 2;
             float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-            if (full || k0 + 3 < nr) {
-              a0 = *reinterpret_cast<const float4*>(yr);
-              a1 = *reinterpret_cast<const float4*>(yr + 4);
-            } else {
-              if (k0 < nr) {
-                a0.x = yr[0];
-                a0.y = yr[1];
-              }
-              if (k0 + 1 < nr) {
-                a0.z = yr[2];
-                a0.w = yr[3];
-              }
-              if (k0 + 2 < nr) {
-                a1.x = yr[4];
-                a1.y = yr[5];
-              }
+            if (k0 < nr) {
+              a0.x = yr[0];
+              a0.y = yr[1];
             }
-            const int fr = 2 * UP + 2 * t;
-            float4 h, l;
-            split(a0.x, h.x, l.x);
-            split(a0.z, h.y, l.y);
-            split(a1.x, h.z, l.z);
-            split(a1.z, h.w, l.w);
-            int off = sw128_off(fr, qd);
-            *reinterpret_cast<float4*>(hi + off) = h;
-            *reinterpret_cast<float4*>(lo + off) = l;
-            split(a0.y, h.x, l.x);
-            split(a0.w, h.y, l.y);
-            split(a1.y, h.z, l.z);
-            split(a1.w, h.w, l.w);
-            off = sw128_off(fr + 1, qd);
-            *reinterpret_cast<float4*>(hi + off) = h;
-            *reinterpret_cast<float4*>(lo + off) = l;
+            if (k0 + 1 < nr) {
+              a0.z = yr[2];
+              a0.w = yr[3];
+            }
+            if (k0 + 2 < nr) {
+              a1.x = yr[4];
+              a1.y = yr[5];
+            }
+            if (k0 + 3 < nr) {
+              a1.z = yr[6];
+              a1.w = yr[7];
+            }
+            const int fr = YB + h * 2 * T + 2 * t;
+            float4 hh, ll;
+            split(a0.x, hh.x, ll.x);
+            split(a0.z, hh.y, ll.y);
+            split(a1.x, hh.z, ll.z);
+            split(a1.z, hh.w, ll.w);
+            *reinterpret_cast<float4*>(hi + sw128_off(fr, qd)) = hh;
+            *reinterpret_cast<float4*>(lo + sw128_off(fr, qd)) = ll;
+            split(a0.y, hh.x, ll.x);
+            split(a0.w, hh.y, ll.y);
+            split(a1.y, hh.z, ll.z);
+            split(a1.w, hh.w, ll.w);
+            *reinterpret_cast<float4*>(hi + sw128_off(fr + 1, qd)) = hh;
+            *reinterpret_cast<float4*>(lo + sw128_off(fr + 1, qd)) = ll;
           }
         }
       }
@@ -591,105 +629,87 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         s = 0;
         ph ^= 1u;
       }
-      if (++j == p.nchunks) {
-        mbar_arrive(&y_empty[y]);  // item's last chunk converted
-        j = 0;
-        ++il;
-      }
+      if (!nul && st.cluster() == upi - 1 && st.j == cpu - 1) mbar_arrive(&y_empty[y]);  // item converted
     }
   } else if (warp < TC_FIRST_SOLVER) {
     // -------------------------------------------------------- assemblers ----
     const int wq = warp & 3;       // TMEM lane quarter this warp may access
     const int m = 32 * wq + lane;  // accumulator row owned by this thread
     const bool odd = (m & 1) != 0;
-    const bool has_rows = 32 * wq < MU;
-    int j = 0, unit = 0, uks = 0;
-    for (int q = 0; q < total; ++q) {
-      const ChunkDesc cd = p.chunks[j];
-      if (++j == p.nchunks) j = 0;
-      uks += (cd.nrows + 7) >> 3;
-      const bool unit_end = (cd.flags & CH_ITEM_END) || (per_cluster && (cd.flags & CH_CLUSTER_END));
-      if (!unit_end) continue;
-      const int nch = (NCH == 6 && uks < 2) ? 3 : NCH;  // chain group 1 untouched
-      uks = 0;
-      const int sv = unit % nsolv;
-      if (unit >= nsolv) wc.wait(&slot_empty[sv], (uint32_t)(((unit / nsolv) - 1) & 1), 1);
-      const int a = unit & 1;
-      wc.wait(&acc_full[a], (uint32_t)((unit >> 1) & 1), 2);
+    // which half / part this row belongs to
+    const int hh = (m < YB) ? m / (2 * UP) : (m - YB) / (2 * T);
+    const bool is_h = m < YB;
+    const bool has_row = m < MU;
+    const bool warp_rows = 32 * wq < MU;
+    for (int v = 0; v < n_pairs; ++v) {
+      const int a = v & 1;
+      // both halves' solver slots must be free before writing either
+      for (int h = 0; h < pair; ++h) {
+        const int u = v * pair + h;
+        if (u < U_tot && u >= nsolv) wc.wait(&slot_empty[u % nsolv], (uint32_t)(((u / nsolv) - 1) & 1), 1);
+      }
+      wc.wait(&acc_full[a], (uint32_t)((v >> 1) & 1), 2);
       tc_fence_after();
-      if (has_rows) {
-        const Work w = work_at(smem, L, sv, UP);
+      const int u_mine = v * pair + hh;
+      if (warp_rows) {
+        const bool write = has_row && u_mine < U_tot;
+        const Work w = work_at(smem, L, u_mine % nsolv, UP);
         float* Gf = reinterpret_cast<float*>(w.G);
         float* Zf = reinterpret_cast<float*>(w.Z);
         const int LD = w.LD;
-        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW);
-        // 16 accumulator columns = 8 UE columns (re, im) per tcgen05.ld; the
-        // partner row (m ^ 1) holds the other component of the same complex row
+        // columns of this row's half: [hh * 2UP, (hh + 1) * 2UP)
+        const uint32_t taddr =
+            tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW + (pair == 2 ? hh : 0) * 2 * UP);
+        const int rloc = is_h ? (m - hh * 2 * UP) : (m - YB - hh * 2 * T);  // row within the half
 #pragma unroll
-        for (int h = 0; h < N / 16; ++h) {
-          float v[16];
-          tmem_ld16(taddr + 16 * h, v);
-          for (int ch = 1; ch < nch; ++ch) {
-            float t16[16];
-            tmem_ld16(taddr + ch * N + 16 * h, t16);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += t16[i];
-          }
+        for (int c16 = 0; c16 < 2 * UP / 16; ++c16) {
+          float vv[16];
+          tmem_ld16(taddr + 16 * c16, vv);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float po = __shfl_xor_sync(0xffffffffu, v[2 * c + 1], 1);
-            const int col = 8 * h + c;
-            if (m < 2 * UP) {
-              const float val = odd ? (po - v[2 * c]) : (v[2 * c] + po);
-              Gf[((m >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
-            } else if (m < MU) {
-              const float val = odd ? (v[2 * c] - po) : (v[2 * c] + po);
-              Zf[(((m - 2 * UP) >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+            const float po = __shfl_xor_sync(0xffffffffu, vv[2 * c + 1], 1);
+            const int col = 8 * c16 + c;
+            if (write) {
+              if (is_h) {
+                const float val = odd ? (po - vv[2 * c]) : (vv[2 * c] + po);
+                Gf[((rloc >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+              } else {
+                const float val = odd ? (vv[2 * c] - po) : (vv[2 * c] + po);
+                Zf[((rloc >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;
+              }
             }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[a]);
-      mbar_arrive(&slot_full[sv]);
-      ++unit;
+      for (int h = 0; h < pair; ++h) {
+        const int u = v * pair + h;
+        if (u < U_tot) mbar_arrive(&slot_full[u % nsolv]);
+      }
     }
   } else {
     // ----------------------------------------------------------- solvers ----
     const int sv = warp - TC_FIRST_SOLVER;
     const Team<32, -1> tm{lane};
     const Work w = work_at(smem, L, sv, UP);
-    int j = 0, unit = 0, il = 0, cl_first = 1;
-    int64_t n = blockIdx.x;
-    for (int q = 0; q < total; ++q) {
-      const ChunkDesc cd = p.chunks[j];
-      const int64_t n_cur = n;
-      const int il_cur = il;
-      if (++j == p.nchunks) {
-        j = 0;
-        n += gridDim.x;
-        ++il;
-      }
-      const bool item_end = (cd.flags & CH_ITEM_END) != 0;
-      const bool unit_end = item_end || (per_cluster && (cd.flags & CH_CLUSTER_END));
-      if (!unit_end) continue;
-      const int my = (unit % nsolv == sv);
-      const int round = unit / nsolv;
-      ++unit;
-      if (!my) continue;
-      wc.wait(&slot_full[sv], (uint32_t)(round & 1), 1);
+    int cl_first = 1;
+    for (int u = sv; u < U_tot; u += nsolv) {
+      const int il = u / upi, c = u % upi;
+      const int64_t n = blockIdx.x + (int64_t)il * gridDim.x;
+      const bool item_end = (c == upi - 1);
+      wc.wait(&slot_full[sv], (uint32_t)((u / nsolv) & 1), 1);
       reset_flags(w, tm);
       tm.sync();
       if (p.ablate & 1) {
       } else if (!fd) {
-        unit_epilogue<UP>(w, p, n_cur, cd.cluster, item_end, cl_first, tm);
+        unit_epilogue<UP>(w, p, n, c, item_end, cl_first, tm);
       } else {
-        const int c = cd.cluster;
         EpiArgs a;
         a.kind = p.kind;
         a.u = p.u;
-        a.T = p.T;
-        a.n0 = item_n0(p, n_cur);
+        a.T = T;
+        a.n0 = item_n0(p, n);
         a.es = p.es;
         a.damping = p.damping;
         a.t_max = p.t_max;
@@ -700,8 +720,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
         else
           linear_unit<UP>(w, a, tm);
-        char* slot = smem + L.items + (il_cur % L.nir) * L.item_stride;
-        fd_fold<UP>(w, slot, IS, p, n_cur, il_cur, c, L.nir, tm);
+        char* slot = smem + L.items + (il % L.nir) * L.item_stride;
+        fd_fold<UP>(w, slot, IS, p, n, il, c, L.nir, tm);
       }
       tm.sync();
       if (lane == 0) mbar_arrive(&slot_empty[sv]);
