@@ -258,6 +258,11 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
   const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count());
+  static float* dtile = nullptr;
+  if (getenv("DBP_TC_DUMP")) {
+    if (!dtile) cudaMalloc(&dtile, 128 * 1024);
+    p.dbg_tile = dtile;
+  }
   static long long* dbg = nullptr;
   const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
   if (debug) {
@@ -266,6 +271,15 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     p.dbg = dbg;
   }
   kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv, ny);
+  if (p.dbg_tile) {
+    static float ht[32768];
+    cudaMemcpy(ht, dtile, L.opb, cudaMemcpyDeviceToHost);
+    FILE* f = fopen("gpurun_out/tile_dump.bin", "wb");
+    if (f) {
+      fwrite(ht, 1, L.opb, f);
+      fclose(f);
+    }
+  }
   if (debug) {
     long long h[20];
     cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);

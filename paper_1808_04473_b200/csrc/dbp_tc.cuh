@@ -398,6 +398,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const int b = pq % TC_NOP;
         const int v = pq / cpu, j = pq - v * cpu;
         wc.wait(&op_full[b], (uint32_t)((pq / TC_NOP) & 1), 1);
+        if (p.dbg_tile && blockIdx.x == 0 && pq == 0) {
+          const float* t = reinterpret_cast<const float*>(smem + L.ops);
+          for (int e = 0; e < L.opb / 4; ++e) p.dbg_tile[e] = t[e];
+        }
         st.v = v;
         st.j = j;
         st.h = 0;
@@ -657,19 +661,22 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         float* Gf = reinterpret_cast<float*>(w.G);
         float* Zf = reinterpret_cast<float*>(w.Z);
         const int LD = w.LD;
-        // columns of this row's half: [hh * 2UP, (hh + 1) * 2UP)
-        const uint32_t taddr =
-            tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW + (pair == 2 ? hh : 0) * 2 * UP);
+        // tcgen05.ld takes one warp-uniform address, and a warp may hold rows of
+        // both halves (e.g. rows 64..95 = Y of half 0 and of half 1): read all
+        // pair * 2UP columns and let each thread keep its half's columns
+        // [hh * 2UP, (hh + 1) * 2UP)
+        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW);
         const int rloc = is_h ? (m - hh * 2 * UP) : (m - YB - hh * 2 * T);  // row within the half
-#pragma unroll
-        for (int c16 = 0; c16 < 2 * UP / 16; ++c16) {
+        for (int c16 = 0; c16 < pair * 2 * UP / 16; ++c16) {
           float vv[16];
           tmem_ld16(taddr + 16 * c16, vv);
+          const int colbase = 8 * c16 - hh * UP;  // UE column of vv[0] within this row's half
+          const bool mine = write && colbase >= 0 && colbase < UP;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const float po = __shfl_xor_sync(0xffffffffu, vv[2 * c + 1], 1);
-            const int col = 8 * c16 + c;
-            if (write) {
+            const int col = colbase + c;
+            if (mine) {
               if (is_h) {
                 const float val = odd ? (po - vv[2 * c]) : (vv[2 * c] + po);
                 Gf[((rloc >> 1) * LD + col) * 2 + (odd ? 1 : 0)] = val;

@@ -48,7 +48,11 @@ def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
     res = grp.run(H, Y, n0)
     ref = dbp.detect(arch, kind, g["H"], g["Y"], g["n0"], [b // c] * c, const, lama_params=lp)
     assert res.items == (0, H.shape[0])
-    assert normwise_rel(res.xhat.cpu().numpy(), ref.xhat) < 2e-6
+    # both sides are fp32 with different Gram summation orders (fused TMEM
+    # accumulation over clusters vs per-cluster stats + reduce-scatter); the
+    # ten LAMA iterations amplify that rounding difference
+    tol = 1e-5 if kind == "lama" else 2e-6
+    assert normwise_rel(res.xhat.cpu().numpy(), ref.xhat) < tol
     assert np.mean(res.decisions.cpu().numpy() != ref.decisions) < 1e-3
     if arch == "fd":
         assert np.max(np.abs(res.nu.cpu().numpy() - ref.nu)) < 2e-6

@@ -1,0 +1,59 @@
+"""dbp_gram_mrc (kernel K1, the tensor-core Gram/MRC stage) against an fp64
+numpy restatement of the per-cluster products G_c = H_c^H H_c, z_c = H_c^H y
+(reference dbp/partial.py, Cluster.gram / Cluster.mrc), over the shapes that
+exercise the operand-tile layouts: two units paired per tcgen05.mma (a warp
+then holds accumulator rows of both units, e.g. Y rows of unit 0 and 1), a
+single unit per tile, per-cluster and cluster-summed outputs, odd and tiny
+T, U=8/16/32 and U=64 (SIMT path)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1808_04473_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # items, B, U, T, offsets, summed
+    (3, 32, 16, 14, [0, 32], 1),
+    (3, 64, 16, 14, [0, 32, 64], 0),
+    (3, 128, 16, 14, [0, 64, 128], 0),
+    (3, 64, 16, 4, [0, 32, 64], 0),
+    (3, 64, 16, 8, [0, 32, 64], 0),
+    (5, 64, 16, 1, [0, 32, 64], 0),
+    (3, 64, 8, 14, [0, 32, 64], 0),
+    (4, 128, 16, 14, [0, 32, 64, 96, 128], 1),
+    (4, 128, 16, 14, [0, 32, 64, 96, 128], 0),
+    (3, 64, 16, 14, [0, 64], 0),
+    (3, 128, 32, 14, [0, 64, 128], 0),
+    (2, 128, 64, 7, [0, 64, 128], 0),
+    (7, 96, 16, 3, [0, 32, 64, 96], 1),
+]
+
+
+@pytest.mark.parametrize("n,b,u,t,offs,summed", CASES)
+def test_gram_mrc_tiles(n, b, u, t, offs, summed):
+    rng = np.random.default_rng(1000 * u + 10 * t + b)
+    H = ((rng.standard_normal((n, b, u)) + 1j * rng.standard_normal((n, b, u))) / 8).astype(np.complex64)
+    Y = (rng.standard_normal((n, t, b)) + 1j * rng.standard_normal((n, t, b))).astype(np.complex64)
+    Hd, Yd = torch.from_numpy(H).cuda(), torch.from_numpy(Y).cuda()
+    c = len(offs) - 1
+    ncl = 1 if summed else c
+    out = torch.full((n, ncl, u * u + t * u), float("nan"), dtype=torch.complex64, device="cuda")
+    offa, offp = _lib.host_i32(offs)  # offa keeps the buffer alive
+    _lib.check(_lib.lib().dbp_gram_mrc(_lib.ptr(Hd), _lib.ptr(Yd), n, b, u, u, t, c, offp, summed,
+                                       _lib.ptr(out), _lib.stream_ptr()))
+    o = out.cpu().numpy()
+    for i in range(n):
+        for k in range(ncl):
+            sl = slice(0, b) if summed else slice(offs[k], offs[k + 1])
+            h = H[i, sl].astype(complex)
+            y = Y[i][:, sl].astype(complex)
+            G = h.conj().T @ h
+            Z = (h.conj().T @ y.T).T
+            scale_g = np.abs(G).max()
+            scale_z = np.abs(Z).max()
+            # 3xTF32 / fp32 accumulation: ~1e-6 relative to the largest entry
+            assert np.abs(o[i, k, :u * u].reshape(u, u) - G).max() < 2e-5 * scale_g, (i, k, "G")
+            assert np.abs(o[i, k, u * u:].reshape(t, u) - Z).max() < 2e-5 * scale_z, (i, k, "Z")
