@@ -218,7 +218,7 @@ template <int UP>
 static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  if (2 * UP + 2 * p.T > 128) return fail(DBP_E_UNSUPPORTED, "2(U+T) > 128 on the tensor-core path");
+  if (2 * UP + 32 > 128) return fail(DBP_E_UNSUPPORTED, "2U + 32 > 128 rows on the tensor-core path");
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -233,7 +233,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     for (int j = 0; j < cpu; ++j)
       if (p.chunks[c * cpu + j].nrows != p.chunks[j].nrows || p.chunks[c * cpu + j].cluster != c) uniform = false;
   if (!uniform) return 1;  // ragged clusters: SIMT kernel
-  p.pair = (2 * (2 * UP + 2 * p.T) <= 128) ? 2 : 1;
+  p.pair = (tc_yrow0(UP, 2) + 2 * 32 <= 128) ? 2 : 1;
   if (const char* e = getenv("DBP_TC_PAIR")) p.pair = std::max(1, std::min(2, atoi(e)));
   // staging depth for ~64 KB of HBM reads in flight per SM (Little's law at
   // ~1.5 us latency), then as many solver warps as shared memory allows
@@ -313,7 +313,7 @@ static int launch_stats(EqParams& p, cudaStream_t st) {
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
   static const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
   const int up = up_for(p.u);
-  if (!force_simt && up <= 32 && 2 * up + 2 * p.T <= 128) {
+  if (!force_simt && up <= 32) {
     int rc = 1;
     switch (up) {
       case 8: rc = launch_tc<8>(p, st); break;

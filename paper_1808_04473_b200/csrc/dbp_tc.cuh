@@ -12,6 +12,15 @@
 // split (x = hi + lo, P = hi.hi + hi.lo + lo.hi) so the result keeps fp32
 // accuracy (plain TF32 would miss the 1e-4 tolerance: SURVEY.md 8(c)).
 //
+// Operand tiles are MN-major with the 128-byte swizzle: one 1 KB atom holds 32
+// features (M or N index, 128 B) of 8 antennas (K).  H is stored [antenna]
+// [features] in HBM, i.e. already MN-major, so its conversion is a row-wise
+// streaming pass; only Y ([symbol][antenna]) is transposed, as (symbol pair,
+// antenna) float4 blocks.  Every converter load and store is conflict-free.
+// M rows of a tile: [H features of the pair's units][Y block of unit 0]
+// [Y block of unit 1], Y blocks 32-row aligned (feature 2t + re/im); the
+// B operand (N) is the H part of the same tile.
+//
 // Roles (one persistent CTA per SM):
 //   warp 0       TMA producer: bulk copies of each chunk (<= 32 antenna rows
 //                of one cluster) of H and Y into a ring of raw stages
@@ -41,11 +50,15 @@ constexpr int TC_CONV = 32 * TC_CONV_W;
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
 
-// byte offset of (feature f, antenna quad qd) in a K=32 operand tile,
-// K-major with the 128-byte swizzle (see umma_desc_sw128)
-__device__ __forceinline__ int sw128_off(int f, int qd) {
-  return (f >> 3) * 1024 + (f & 7) * 128 + ((qd ^ (f & 7)) << 4);
+// byte offset of (M row f, antenna kr) in an operand tile: MN-major tf32
+// (128-byte rows, 32-byte granules swizzled by kr % 4; umma_desc_mn_sw128),
+// M blocks of 32 rows `lbo` bytes apart, antenna rows 128 B apart; f is
+// 4-aligned (one 16-byte chunk = 4 consecutive M rows of one antenna)
+__device__ __forceinline__ int mn_off(int f, int kr, int lbo) {
+  return (f >> 5) * lbo + kr * 128 + ((((f & 31) >> 3) ^ (kr & 3)) << 5) + (f & 4) * 4;
 }
+// first M row of the Y blocks
+__host__ __device__ constexpr int tc_yrow0(int UP, int pair) { return ((pair * 2 * UP + 31) / 32) * 32; }
 
 // FD item ring slot: the fusion sums of one item, folded cluster by cluster.
 struct ItemSlotLayout {
@@ -71,7 +84,7 @@ __host__ __device__ inline ItemSlotLayout make_item_slot(int UP, int TP, int C) 
 }
 
 struct TcLayout {
-  int bars, tmem_slot, hst, hbytes, yst, ybytes, ops, opb, slack, work, work_stride, items, item_stride, nir, total;
+  int bars, tmem_slot, hst, hbytes, yst, ybytes, ops, opb, lbo, work, work_stride, items, item_stride, nir, total;
   WorkLayout w;  // offsets relative to a solver's work base
 };
 
@@ -81,7 +94,6 @@ struct TcLayout {
 __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B, int us, int KC, int NS, int NY,
                                                    int C, bool lama, bool fd, int nsolv, int pair) {
   TcLayout L;
-  const int MB = (pair * (2 * UP + 2 * T) + 7) / 8;  // 8-row core-matrix blocks used
   int o = 0;
   L.bars = o;
   o += (2 * NS + 2 * NY + 2 * TC_NOP + 4 + 2 * TC_MAX_SOLV) * 8;
@@ -96,7 +108,8 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B,
   o += NY * L.ybytes;
   o = align_up(o, 1024);
   L.ops = o;
-  L.opb = MB * 1024;  // one K=32 tile: MB blocks x 8 k-quads x 128 B
+  L.lbo = (KC / 8) * 1024;  // one 32-row M block of a K=KC tile
+  L.opb = 4 * L.lbo;        // 4 M blocks = the 128 rows one MMA reads
   o += 2 * TC_NOP * L.opb;  // [hi0][lo0][hi1][lo1]...
   L.work = o;
   L.w = make_work_layout(0, UP, TP, C, lama, false);
@@ -107,12 +120,6 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B,
   L.item_stride = S.total;
   L.nir = fd ? (nsolv + C - 1) / C + 2 : 0;
   o += L.nir * L.item_stride;
-  // the M=128 MMA reads 16 blocks (16 KB) from each tile base; rows past
-  // MB*8 are never written and only produce ignored accumulator rows, but
-  // they must stay inside the CTA's shared memory
-  const int after_last = o - (L.work - L.opb);
-  L.slack = (after_last < 16 * 1024) ? 16 * 1024 - after_last : 0;
-  o += L.slack;
   L.total = align_up(o, 128);
   return L;
 }
@@ -286,9 +293,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const int NS = p.NS;
   const int NY = ny;
   const int T = p.T;
-  const int YB = pair * 2 * UP;          // first Y row of the tile
-  const int MU = YB + pair * 2 * T;      // rows in use
-  const int MB = (MU + 7) / 8;
+  const int HR = pair * 2 * UP;          // H rows of the tile (= MMA N)
+  const int YB = tc_yrow0(UP, pair);     // first Y row (32-aligned)
+  const int MU = YB + pair * 32;         // rows in use
   const TcLayout L = make_tc_layout(UP, p.TP, T, p.B, p.us, p.KC, NS, NY, p.C, lama, fd, nsolv, pair);
   const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // H chunk ring
@@ -332,6 +339,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     f[1] = 0x7fffffff;
     f[2] = k * p.C;  // turn: first cluster of CTA-local item k
   }
+  // operand tiles start zeroed: pad features (odd U, T < 16) and unused M
+  // blocks are never written afterwards
+  for (int e = tid; e < 2 * TC_NOP * L.opb / 16; e += blockDim.x)
+    reinterpret_cast<float4*>(smem + L.ops)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -391,7 +402,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer ----
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc_tf32(128, N);
+      const uint32_t idesc = umma_idesc_tf32_mn(128, N);
+      const uint32_t lbo = (uint32_t)L.lbo;
       const uint32_t ops = smem_u32(smem + L.ops);
       Stream st = s0;
       for (int pq = 0; pq < S_tot / pair; ++pq) {  // one tile per (pair v, chunk j)
@@ -415,8 +427,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const int nk8 = (p.ablate & 2) ? 0 : (cd.nrows + 7) >> 3;
         for (int ks = 0; ks < nk8; ++ks) {
           const uint32_t acc = (j == 0 && ks == 0) ? 0u : 1u;
-          const uint64_t ah = umma_desc_sw128(hi + ks * 32, 1024);
-          const uint64_t al = umma_desc_sw128(lo + ks * 32, 1024);
+          const uint64_t ah = umma_desc_mn_sw128(hi + ks * 1024, lbo, 512);
+          const uint64_t al = umma_desc_mn_sw128(lo + ks * 1024, lbo, 512);
           umma_tf32(d, ah, ah, idesc, acc);
           umma_tf32(d, ah, al, idesc, 1u);
           umma_tf32(d, al, ah, idesc, 1u);
@@ -429,63 +441,31 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   } else if (warp < 2 + TC_CONV_W) {
     // -------------------------------------------------------- converters ----
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
-    // Tile layout (K-major, 128-byte swizzle): row f, antenna k ->
-    // (f/8)*1024 + (f%8)*128 + ((k/4) ^ (f%8))*16 + (k%4)*4 bytes.  H tasks move
-    // a 4-feature x 4-antenna block (4x4 transpose in registers), Y tasks one
-    // symbol's (re, im) rows x 4 antennas.
+    // H rows: one float4 (2 UEs) per task, written to the same antenna row of
+    // the tile (4 rows x 8 chunks per warp: one wavefront per row).  Y: task
+    // (symbol pair tp, antenna pair) reads Y[2tp][k..k+1] and Y[2tp+1][k..k+1]
+    // and writes chunk tp of antenna rows k and k+1.  Pad rows/features of
+    // the tiles were zeroed at kernel start and are never written.
     const int ct = tid - 64;
     const int us2 = 2 * p.us;
-    constexpr int HG = UP / 2;  // 4-feature groups of the H part of one half
-    // rows past the ones in use, and H columns past the stored row width
-    // (odd U), are zero forever
-    for (int e = ct; e < 2 * TC_NOP * MB * 8 * 8; e += TC_CONV) {
-      const int buf = e / (MB * 64), r = e % (MB * 64);
-      const int f = r / 8, qd = r % 8;
-      const bool hpad = f < YB && (f % (2 * UP)) >= us2;
-      if (f >= MU || hpad)
-        *reinterpret_cast<float4*>(smem + L.ops + buf * L.opb + sw128_off(f, qd)) =
-            make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    const int hq = p.us / 2;             // float4 per stored H row
+    constexpr int HQ = UP / 2;           // float4 slots per H row of the tile
+    const int lbo = L.lbo;
+    const int tpairs = (T + 1) / 2;
+    const int yrow = 2 * p.B;            // floats per Y symbol row
     auto split = [](float x, float& h, float& l) {
       h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
       l = x - h;
     };
-    // static task list of this thread for a full KC=32-row chunk of one half:
-    // task = (group g, antenna quad qd); g < HG: H features 4g..4g+3, else
-    // symbol t = g - HG (re, im rows); store offsets for half 0 (half 1 adds
-    // the row shift, which keeps the swizzle phase: shifts are multiples of 8)
-    const int ng = HG + T;
-    constexpr int MAXT = 2;  // (UP/2 + T) * 8 <= 2 * TC_CONV for UP <= 32, T <= 16
-    int t_ld[MAXT], t_kind[MAXT], t_st[MAXT][4];
-#pragma unroll
-    for (int r = 0; r < MAXT; ++r) {
-      const int task = ct + r * TC_CONV;
-      t_kind[r] = -1;
-      t_ld[r] = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) t_st[r][c] = 0;
-      if (task < ng * 8) {
-        const int qd = task / ng, g = task - qd * ng;
-        if (g < HG) {
-          if (4 * g < us2) {
-            t_kind[r] = 0;
-            t_ld[r] = 4 * qd * us2 + 4 * g;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) t_st[r][c] = sw128_off(4 * g + c, qd);
-          }
-        } else {
-          const int t = g - HG;
-          t_kind[r] = 1;
-          t_ld[r] = (t * p.B + 4 * qd) * 2;
-          // (re, im) rows of symbol t for half 0 and half 1 (a 2T-row shift
-          // need not preserve the swizzle phase, so both are precomputed)
-          t_st[r][0] = sw128_off(YB + 2 * t, qd);
-          t_st[r][1] = sw128_off(YB + 2 * t + 1, qd);
-          t_st[r][2] = sw128_off(YB + 2 * T + 2 * t, qd);
-          t_st[r][3] = sw128_off(YB + 2 * T + 2 * t + 1, qd);
-        }
-      }
-    }
+    auto put = [&](char* hi, char* lo, int off, float4 v) {
+      float4 hh, ll;
+      split(v.x, hh.x, ll.x);
+      split(v.y, hh.y, ll.y);
+      split(v.z, hh.z, ll.z);
+      split(v.w, hh.w, ll.w);
+      *reinterpret_cast<float4*>(hi + off) = hh;
+      *reinterpret_cast<float4*>(lo + off) = ll;
+    };
     Stream st = s0;
     int s = 0;
     uint32_t ph = 0;
@@ -499,131 +479,42 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       wc.wait(&raw_full[s], ph, 1);
       if (!nul) wc.wait(&y_full[y], (uint32_t)((il / NY) & 1), 2);
       if (h == 0 && pq >= TC_NOP) wc.wait(&op_empty[b], (uint32_t)(((pq / TC_NOP) - 1) & 1), 3);
-      const ChunkDesc cd = p.chunks[st.chunk_index()];
-      const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
-      const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
-      char* hi = smem + L.ops + 2 * b * L.opb;
-      char* lo = hi + L.opb;
-      // half h: H rows shift by h*2UP (a multiple of 8 rows: same swizzle
-      // phase); Y rows use the per-half precomputed offsets
-      const int hshift = h * 2 * UP * 128;
-      if (nul) {
-        for (int e = ct; e < (2 * UP + 2 * T) * 8; e += TC_CONV) {
-          const int r = e / 8, qd = e % 8;
-          const int f = (r < 2 * UP) ? h * 2 * UP + r : YB + h * 2 * T + (r - 2 * UP);
-          *reinterpret_cast<float4*>(hi + sw128_off(f, qd)) = make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4*>(lo + sw128_off(f, qd)) = make_float4(0.f, 0.f, 0.f, 0.f);
+      // a null half (odd unit count) is left as is: its rows and columns of
+      // the accumulator are never read, and rows/columns do not mix
+      if (!nul && !(p.ablate & 4)) {
+        const ChunkDesc cd = p.chunks[st.chunk_index()];
+        const int nr = cd.nrows, nr8 = (nr + 7) & ~7;
+        const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
+        const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
+        char* hi = smem + L.ops + 2 * b * L.opb;
+        char* lo = hi + L.opb;
+        const int fh = h * 2 * UP;             // first M row of this unit's H features
+        const int fy = YB + 32 * h;            // first M row of this unit's Y block
+        for (int e = ct; e < nr8 * HQ; e += TC_CONV) {
+          const int kr = e / HQ, c4 = e % HQ;
+          if (c4 >= hq) continue;
+          const float4 v = (kr < nr) ? *reinterpret_cast<const float4*>(Hf + kr * us2 + 4 * c4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          put(hi, lo, mn_off(fh + 4 * c4, kr, lbo), v);
         }
-      } else if (cd.nrows == 32 && !(p.ablate & 4)) {
-#pragma unroll
-        for (int r = 0; r < MAXT; ++r) {
-          if (t_kind[r] < 0) continue;
-          if (t_kind[r] == 0) {
-            const float* src = Hf + t_ld[r];
-            const float4 r0 = *reinterpret_cast<const float4*>(src);
-            const float4 r1 = *reinterpret_cast<const float4*>(src + us2);
-            const float4 r2 = *reinterpret_cast<const float4*>(src + 2 * us2);
-            const float4 r3 = *reinterpret_cast<const float4*>(src + 3 * us2);
-            const float cols[4][4] = {{r0.x, r1.x, r2.x, r3.x}, {r0.y, r1.y, r2.y, r3.y},
-                                      {r0.z, r1.z, r2.z, r3.z}, {r0.w, r1.w, r2.w, r3.w}};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float4 hh, ll;
-              split(cols[c][0], hh.x, ll.x);
-              split(cols[c][1], hh.y, ll.y);
-              split(cols[c][2], hh.z, ll.z);
-              split(cols[c][3], hh.w, ll.w);
-              const int off = t_st[r][c] + hshift;
-              *reinterpret_cast<float4*>(hi + off) = hh;
-              *reinterpret_cast<float4*>(lo + off) = ll;
-            }
-          } else {
-            const float* yr = Yf + t_ld[r];
-            const float4 a0 = *reinterpret_cast<const float4*>(yr);
-            const float4 a1 = *reinterpret_cast<const float4*>(yr + 4);
-            float4 hh, ll;
-            split(a0.x, hh.x, ll.x);
-            split(a0.z, hh.y, ll.y);
-            split(a1.x, hh.z, ll.z);
-            split(a1.z, hh.w, ll.w);
-            const int o_re = h ? t_st[r][2] : t_st[r][0];
-            const int o_im = h ? t_st[r][3] : t_st[r][1];
-            *reinterpret_cast<float4*>(hi + o_re) = hh;
-            *reinterpret_cast<float4*>(lo + o_re) = ll;
-            split(a0.y, hh.x, ll.x);
-            split(a0.w, hh.y, ll.y);
-            split(a1.y, hh.z, ll.z);
-            split(a1.w, hh.w, ll.w);
-            *reinterpret_cast<float4*>(hi + o_im) = hh;
-            *reinterpret_cast<float4*>(lo + o_im) = ll;
+        // Y tasks: a warp takes 4 symbol pairs x 8 antenna pairs, so its loads
+        // are 4 full 128-byte row segments and its stores hit all 8 chunk
+        // positions of the swizzle 4 times each (4 wavefronts, the minimum)
+        const int kb8 = (nr8 / 2 + 7) / 8;    // 8-antenna-pair blocks
+        const int ntask = 32 * kb8 * ((tpairs + 3) / 4);
+        for (int e = ct; e < ntask; e += TC_CONV) {
+          const int blk = e >> 5;
+          const int tp = 4 * (blk / kb8) + ((e >> 3) & 3);
+          const int k = 2 * ((e & 7) + 8 * (blk % kb8));
+          if (tp >= tpairs || k >= nr8) continue;
+          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+          if (k < nr) {
+            a0 = *reinterpret_cast<const float4*>(Yf + 2 * tp * yrow + 2 * k);
+            if (2 * tp + 1 < T) a1 = *reinterpret_cast<const float4*>(Yf + (2 * tp + 1) * yrow + 2 * k);
           }
-        }
-      } else {
-        // generic chunk (fewer rows, or rows not a multiple of 8): zero-pad K
-        const int nr = cd.nrows;
-        const int nq = 2 * ((nr + 7) >> 3);
-        const int ntask = (p.ablate & 4) ? 0 : ng * nq;
-        for (int task = ct; task < ntask; task += TC_CONV) {
-          const int qd = task / ng;
-          const int g = task - qd * ng;
-          const int k0 = 4 * qd;
-          if (g < HG) {
-            const int f0 = 4 * g;
-            float4 r4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int k = k0 + i;
-              r4[i] = (f0 < us2 && k < nr) ? *reinterpret_cast<const float4*>(Hf + k * us2 + f0)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float cols[4][4] = {{r4[0].x, r4[1].x, r4[2].x, r4[3].x}, {r4[0].y, r4[1].y, r4[2].y, r4[3].y},
-                                      {r4[0].z, r4[1].z, r4[2].z, r4[3].z}, {r4[0].w, r4[1].w, r4[2].w, r4[3].w}};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              float4 hh, ll;
-              split(cols[c][0], hh.x, ll.x);
-              split(cols[c][1], hh.y, ll.y);
-              split(cols[c][2], hh.z, ll.z);
-              split(cols[c][3], hh.w, ll.w);
-              const int off = sw128_off(h * 2 * UP + f0 + c, qd);
-              *reinterpret_cast<float4*>(hi + off) = hh;
-              *reinterpret_cast<float4*>(lo + off) = ll;
-            }
-          } else {
-            const int t = g - HG;
-            const float* yr = Yf + (t * p.B + k0) * 2;
-            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-            if (k0 < nr) {
-              a0.x = yr[0];
-              a0.y = yr[1];
-            }
-            if (k0 + 1 < nr) {
-              a0.z = yr[2];
-              a0.w = yr[3];
-            }
-            if (k0 + 2 < nr) {
-              a1.x = yr[4];
-              a1.y = yr[5];
-            }
-            if (k0 + 3 < nr) {
-              a1.z = yr[6];
-              a1.w = yr[7];
-            }
-            const int fr = YB + h * 2 * T + 2 * t;
-            float4 hh, ll;
-            split(a0.x, hh.x, ll.x);
-            split(a0.z, hh.y, ll.y);
-            split(a1.x, hh.z, ll.z);
-            split(a1.z, hh.w, ll.w);
-            *reinterpret_cast<float4*>(hi + sw128_off(fr, qd)) = hh;
-            *reinterpret_cast<float4*>(lo + sw128_off(fr, qd)) = ll;
-            split(a0.y, hh.x, ll.x);
-            split(a0.w, hh.y, ll.y);
-            split(a1.y, hh.z, ll.z);
-            split(a1.w, hh.w, ll.w);
-            *reinterpret_cast<float4*>(hi + sw128_off(fr + 1, qd)) = hh;
-            *reinterpret_cast<float4*>(lo + sw128_off(fr + 1, qd)) = ll;
-          }
+          const int f = fy + 4 * tp;
+          put(hi, lo, mn_off(f, k, lbo), make_float4(a0.x, a0.y, a1.x, a1.y));
+          put(hi, lo, mn_off(f, k + 1, lbo), make_float4(a0.z, a0.w, a1.z, a1.w));
         }
       }
       fence_proxy_async_smem();
@@ -641,9 +532,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const int m = 32 * wq + lane;  // accumulator row owned by this thread
     const bool odd = (m & 1) != 0;
     // which half / part this row belongs to
-    const int hh = (m < YB) ? m / (2 * UP) : (m - YB) / (2 * T);
-    const bool is_h = m < YB;
-    const bool has_row = m < MU;
+    const bool is_h = m < HR;
+    const int hh = is_h ? m / (2 * UP) : (m - YB) / 32;
+    const bool has_row = is_h || (m >= YB && m < MU && ((m - YB) & 31) < 2 * T);
     const bool warp_rows = 32 * wq < MU;
     for (int v = 0; v < n_pairs; ++v) {
       const int a = v & 1;
@@ -666,7 +557,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         // pair * 2UP columns and let each thread keep its half's columns
         // [hh * 2UP, (hh + 1) * 2UP)
         const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW);
-        const int rloc = is_h ? (m - hh * 2 * UP) : (m - YB - hh * 2 * T);  // row within the half
+        const int rloc = is_h ? (m - hh * 2 * UP) : ((m - YB) & 31);  // row within the half
         for (int c16 = 0; c16 < pair * 2 * UP / 16; ++c16) {
           float vv[16];
           tmem_ld16(taddr + 16 * c16, vv);
