@@ -14,7 +14,8 @@ import threading
 from .errors import BackendError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbp_b200.so")
+# DBP_LIB: alternative build of the same library (A/B timing studies only)
+LIB_PATH = os.environ.get("DBP_LIB") or os.path.join(_HERE, "libdbp_b200.so")
 ABI_VERSION = 1
 
 # status codes (include/dbp_b200.h)

@@ -47,6 +47,10 @@ struct EqParams {
   float2 *tr_z, *tr_s, *tr_v;
   float* tr_phi;
   int pair;        // tensor-core kernel: units per operand tile (1 or 2)
+  // tensor-core kernel staging: a stage is `ips` consecutive whole items
+  // (spi == 1) or one row block of one item (spi > 1); H part then Y part
+  int ips, spi, stage_bytes, stage_hbytes;
+  int st_row0[MAX_SPI], st_rows[MAX_SPI];
   float* dbg_tile;  // debug: first operand tile of CTA 0 (DBP_TC_DUMP)
   long long* dbg;  // debug: per-role wait-cycle counters [5][4] (DBP_TC_DEBUG)
   int ablate;  // debug: 1 skip solver work, 2 skip MMAs, 4 skip conversion (timing studies only)

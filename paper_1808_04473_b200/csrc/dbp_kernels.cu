@@ -233,25 +233,83 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     for (int j = 0; j < cpu; ++j)
       if (p.chunks[c * cpu + j].nrows != p.chunks[j].nrows || p.chunks[c * cpu + j].cluster != c) uniform = false;
   if (!uniform) return 1;  // ragged clusters: SIMT kernel
+  // pair two units per tile when M allows; per-cluster units pair within an
+  // item (even cluster count), items pair within a stage
   p.pair = (tc_yrow0(UP, 2) + 2 * 32 <= 128) ? 2 : 1;
+  if (upi > 1 && (upi & 1)) p.pair = 1;
   if (const char* e = getenv("DBP_TC_PAIR")) p.pair = std::max(1, std::min(2, atoi(e)));
-  // staging depth for ~64 KB of HBM reads in flight per SM (Little's law at
-  // ~1.5 us latency), then as many solver warps as shared memory allows
-  const int ybytes = p.T * p.B * 8;
-  int ny = p.pair == 2 ? 4 : (ybytes <= 16384 ? 3 : 2);
-  p.NS = std::max(4, std::min(12, (64 * 1024 - ny * ybytes) / (p.KC * p.us * 8)));
-  auto fits = [&](int ns, int nyy, int nsv) {
-    return make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, ns, nyy, p.C, lama, fd, nsv, p.pair).total <= smem_max;
+  // staging plan: whole items (several per stage when small) or row blocks
+  const int hrow = p.us * 8, yrow = p.T * 8;  // bytes per antenna row of H / Y
+  const int item_bytes = p.B * (hrow + yrow);
+  int smax = 64 * 1024;
+  if (const char* e = getenv("DBP_TC_SMAX")) smax = atoi(e) * 1024;
+  if (p.pair == 2 && upi == 1 && 2 * item_bytes > smax) p.pair = 1;  // item pairs must share a stage
+  const int step = (p.pair == 2 && upi == 1) ? 2 : 1;
+  if (item_bytes <= smax) {
+    p.spi = 1;
+    p.ips = std::max(step, (smax / item_bytes) / step * step);
+    p.st_row0[0] = 0;
+    p.st_rows[0] = p.B;
+  } else {
+    // row blocks at chunk boundaries (cluster-pair boundaries when units pair
+    // inside an item), each at most smax bytes
+    p.ips = 1;
+    p.spi = 0;
+    const int unit_step = (p.pair == 2 && upi > 1) ? 2 : 1;
+    int r0 = 0, rows = 0;
+    for (int j = 0; j < p.nchunks; ++j) {
+      const ChunkDesc& cd = p.chunks[j];
+      const bool boundary = (cd.row0 == p.chunks[(cd.cluster / unit_step) * unit_step * cpu].row0) || !per_cluster;
+      if (rows > 0 && boundary && (rows + cd.nrows) * (hrow + yrow) > smax) {
+        if (p.spi == MAX_SPI) return 1;
+        p.st_row0[p.spi] = r0;
+        p.st_rows[p.spi++] = rows;
+        r0 = cd.row0;
+        rows = 0;
+      }
+      rows += cd.nrows;
+    }
+    if (p.spi == MAX_SPI) return 1;
+    p.st_row0[p.spi] = r0;
+    p.st_rows[p.spi++] = rows;
+  }
+  int rmax = 0;
+  for (int k = 0; k < p.spi; ++k) rmax = std::max(rmax, p.st_rows[k]);
+  p.stage_hbytes = p.ips * rmax * hrow;
+  p.stage_bytes = p.stage_hbytes + p.ips * rmax * yrow;
+  // chunk -> stage, and the last chunk of the item's visit order touching
+  // each stage (units of an item in order; paired clusters interleave)
+  for (int j = 0; j < p.nchunks; ++j) {
+    int k = 0;
+    while (k + 1 < p.spi && p.chunks[j].row0 >= p.st_row0[k + 1]) ++k;
+    p.chunks[j].flags = (p.chunks[j].flags & 0xff) | (k << CH_STAGE_SHIFT);
+  }
+  {
+    int last[MAX_SPI];
+    for (int k = 0; k < MAX_SPI; ++k) last[k] = -1;
+    const int ps = (p.pair == 2 && upi > 1) ? 2 : 1;  // units of an item sharing a tile
+    for (int c0 = 0; c0 < upi; c0 += ps)
+      for (int j = 0; j < cpu; ++j)
+        for (int h = 0; h < ps; ++h) {
+          const int idx = (c0 + h) * cpu + j;
+          last[(p.chunks[idx].flags >> CH_STAGE_SHIFT) & 0xff] = idx;
+        }
+    for (int k = 0; k < p.spi; ++k)
+      if (last[k] >= 0) p.chunks[last[k]].flags |= CH_STAGE_REL;
+  }
+  auto fits = [&](int ns, int nsv) {
+    return make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, ns, p.C, lama, fd, nsv).total <= smem_max;
   };
+  // ring depth: ~96 KB of stages when they fit (>= 2), then solver warps
+  p.NS = std::max(2, std::min(8, (96 * 1024 + p.stage_bytes - 1) / p.stage_bytes));
   int nsolv = TC_MAX_SOLV;
   // tuning overrides (timing studies only)
   if (const char* e = getenv("DBP_TC_NS")) p.NS = atoi(e);
-  if (const char* e = getenv("DBP_TC_NY")) ny = atoi(e);
   if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(2, std::min(TC_MAX_SOLV, atoi(e)));
-  while (nsolv > 2 && !fits(p.NS, ny, nsolv)) --nsolv;
-  while (p.NS > 3 && !fits(p.NS, ny, nsolv)) --p.NS;
-  while (ny > 2 && !fits(p.NS, ny, nsolv)) --ny;
-  const TcLayout L = make_tc_layout(UP, p.TP, p.T, p.B, p.us, p.KC, p.NS, ny, p.C, lama, fd, nsolv, p.pair);
+  while (nsolv > 4 && !fits(p.NS, nsolv)) --nsolv;
+  while (p.NS > 2 && !fits(p.NS, nsolv)) --p.NS;
+  while (nsolv > 2 && !fits(p.NS, nsolv)) --nsolv;
+  const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, p.NS, p.C, lama, fd, nsolv);
   if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
   auto kern = tc_kernel<UP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
@@ -266,11 +324,11 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   static long long* dbg = nullptr;
   const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
   if (debug) {
-    if (!dbg) cudaMalloc(&dbg, 20 * sizeof(long long));
-    cudaMemsetAsync(dbg, 0, 20 * sizeof(long long), st);
+    if (!dbg) cudaMalloc(&dbg, 128 * sizeof(long long));
+    cudaMemsetAsync(dbg, 0, 128 * sizeof(long long), st);
     p.dbg = dbg;
   }
-  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv, ny);
+  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv);
   if (p.dbg_tile) {
     static float ht[32768];
     cudaMemcpy(ht, dtile, L.opb, cudaMemcpyDeviceToHost);
@@ -281,14 +339,16 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     }
   }
   if (debug) {
-    long long h[20];
+    long long h[128];
     cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
-    static const char* names[5] = {"producer", "mma", "converter", "assembler", "solver"};
-    fprintf(stderr, "[dbp tc debug] NS=%d NY=%d nsolv=%d (cycles summed over CTAs, one lane per role)\n", p.NS, ny,
-            nsolv);
-    for (int r = 0; r < 5; ++r)
-      fprintf(stderr, "  %-9s total %.3e  wait1 %.3e  wait2 %.3e  wait3 %.3e\n", names[r], (double)h[r * 4],
-              (double)h[r * 4 + 1], (double)h[r * 4 + 2], (double)h[r * 4 + 3]);
+    fprintf(stderr, "[dbp tc debug] NS=%d stage=%d B ips=%d spi=%d pair=%d nsolv=%d (cycles summed over CTAs)\n",
+            p.NS, p.stage_bytes, p.ips, p.spi, p.pair, nsolv);
+    for (int w = 0; w < threads / 32; ++w) {
+      const char* name = w == 0 ? "producer" : w == 1 ? "mma" : w < 2 + TC_CONV_W ? "converter"
+                         : w < TC_FIRST_SOLVER ? "assembler" : "solver";
+      fprintf(stderr, "  w%-2d %-9s total %.3e  c1 %.3e  c2 %.3e  c3 %.3e\n", w, name, (double)h[w * 4],
+              (double)h[w * 4 + 1], (double)h[w * 4 + 2], (double)h[w * 4 + 3]);
+    }
   }
   return cuda_check("tc_kernel");
 }

@@ -45,7 +45,7 @@ constexpr int TC_CONV_W = 4;  // converter warps (2..5)
 constexpr int TC_ASM_W = 4;   // assembler warps (6..9)
 constexpr int TC_FIRST_SOLVER = 2 + TC_CONV_W + TC_ASM_W;
 constexpr int TC_MAX_SOLV = 6;
-constexpr int TC_NOP = 4;  // operand tile ring depth (converter -> MMA)
+constexpr int TC_NOP = 2;  // operand tile ring depth (converter -> MMA)
 constexpr int TC_CONV = 32 * TC_CONV_W;
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
@@ -84,28 +84,27 @@ __host__ __device__ inline ItemSlotLayout make_item_slot(int UP, int TP, int C) 
 }
 
 struct TcLayout {
-  int bars, tmem_slot, hst, hbytes, yst, ybytes, ops, opb, lbo, work, work_stride, items, item_stride, nir, total;
+  int bars, tmem_slot, chunks, stg, sbytes, ops, opb, lbo, work, work_stride, items, item_stride, nir, total;
   WorkLayout w;  // offsets relative to a solver's work base
 };
 
-// Raw staging: a ring of NS H chunks (KC antenna rows each, one bulk copy)
-// and a ring of NY whole-item Y blocks (T x B, one bulk copy per item -- the
-// per-symbol rows of a chunk are only 8*KC bytes and would cost T tiny copies).
-__host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int T, int B, int us, int KC, int NS, int NY,
-                                                   int C, bool lama, bool fd, int nsolv, int pair) {
+// Raw staging: a ring of NS stages, each `sbytes` of H rows then Y rows of
+// `ips` consecutive items (or one row block of an item), filled by 2 bulk
+// copies (whole items) or 1 + T copies (row block); then the operand tiles.
+__host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int sbytes, int KC, int NS, int C, bool lama,
+                                                   bool fd, int nsolv) {
   TcLayout L;
   int o = 0;
   L.bars = o;
-  o += (2 * NS + 2 * NY + 2 * TC_NOP + 4 + 2 * TC_MAX_SOLV) * 8;
+  o += (2 * NS + 2 * TC_NOP + 4 + 2 * TC_MAX_SOLV) * 8;
   L.tmem_slot = o;
   o += 16;
+  L.chunks = o;  // copy of the chunk table (+ stage rows): dynamic param loads are slow
+  o += (MAX_CHUNKS + 2 * MAX_SPI) * 16;
   o = align_up(o, 128);
-  L.hbytes = align_up(KC * us * 8, 128);
-  L.hst = o;
-  o += NS * L.hbytes;
-  L.ybytes = align_up(T * B * 8, 128);
-  L.yst = o;
-  o += NY * L.ybytes;
+  L.sbytes = align_up(sbytes, 128);
+  L.stg = o;
+  o += NS * L.sbytes;
   o = align_up(o, 1024);
   L.ops = o;
   L.lbo = (KC / 8) * 1024;  // one 32-row M block of a K=KC tile
@@ -279,8 +278,7 @@ struct Stream {
 };
 
 template <int UP>
-__global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv,
-                                                                int ny) {
+__global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv) {
   extern __shared__ __align__(1024) char smem[];
   const int pair = p.pair;
   const int N = pair * 2 * UP;  // MMA N: the H features of both halves
@@ -291,36 +289,37 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   const int NS = p.NS;
-  const int NY = ny;
   const int T = p.T;
   const int HR = pair * 2 * UP;          // H rows of the tile (= MMA N)
   const int YB = tc_yrow0(UP, pair);     // first Y row (32-aligned)
   const int MU = YB + pair * 32;         // rows in use
-  const TcLayout L = make_tc_layout(UP, p.TP, T, p.B, p.us, p.KC, NS, NY, p.C, lama, fd, nsolv, pair);
+  const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, NS, p.C, lama, fd, nsolv);
   const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
-  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // H chunk ring
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // stage ring
   uint64_t* raw_empty = raw_full + NS;
-  uint64_t* y_full = raw_empty + NS;  // Y item ring
-  uint64_t* y_empty = y_full + NY;
-  uint64_t* op_full = y_empty + NY;
+  uint64_t* op_full = raw_empty + NS;
   uint64_t* op_empty = op_full + TC_NOP;
   uint64_t* acc_full = op_empty + TC_NOP;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* slot_full = acc_empty + 2;
   uint64_t* slot_empty = slot_full + TC_MAX_SOLV;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+  ChunkDesc* chunks = reinterpret_cast<ChunkDesc*>(smem + L.chunks);
+  int* st_row0 = reinterpret_cast<int*>(chunks + MAX_CHUNKS);
+  int* st_rows = st_row0 + MAX_SPI;
+  for (int e = threadIdx.x; e < p.nchunks; e += blockDim.x) chunks[e] = p.chunks[e];
+  for (int e = threadIdx.x; e < MAX_SPI; e += blockDim.x) {
+    st_row0[e] = p.st_row0[e];
+    st_rows[e] = p.st_rows[e];
+  }
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&raw_full[s], 1);
       mbar_init(&raw_empty[s], TC_CONV);
     }
-    for (int y = 0; y < NY; ++y) {
-      mbar_init(&y_full[y], 1);
-      mbar_init(&y_empty[y], TC_CONV);
-    }
     for (int b = 0; b < TC_NOP; ++b) {
-      mbar_init(&op_full[b], TC_CONV * pair);
+      mbar_init(&op_full[b], TC_CONV);
       mbar_init(&op_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -349,7 +348,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t my_items = (p.n_items > blockIdx.x) ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // a contiguous range of items per CTA (so a stage can hold consecutive items)
+  const int64_t per_cta = p.n_items / gridDim.x, extra = p.n_items % gridDim.x;
+  const int64_t first = blockIdx.x * per_cta + min((int64_t)blockIdx.x, extra);
+  const int64_t my_items = per_cta + (blockIdx.x < extra ? 1 : 0);
   const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
   const int upi = per_cluster ? p.C : 1;
   const int cpu = p.nchunks / upi;
@@ -357,40 +359,42 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const int n_pairs = (U_tot + pair - 1) / pair;
   const int S_tot = n_pairs * pair * cpu;  // stream length
   const Stream s0{pair, cpu, upi, U_tot, 0, 0, 0};
-  // role id for the debug counters: 0 producer, 1 mma, 2 converter, 3 assembler, 4 solver
-  const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp < 2 + TC_CONV_W ? 2 : warp < TC_FIRST_SOLVER ? 3 : 4;
-  const bool rec = p.dbg && lane == 0 && (warp < 3 || warp == 2 + TC_CONV_W || warp == TC_FIRST_SOLVER);
+  const bool rec = p.dbg && lane == 0;
   long long cnt[4] = {0, 0, 0, 0};
   WaitClock wc{rec ? cnt : nullptr};
   const long long t_start = clock64();
 
+  const int ips = p.ips, spi = p.spi;
+  const int n_groups = (int)((my_items + ips - 1) / ips);
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer ----
-    if (lane == 0) {
-      const uint64_t policy = l2_evict_first_policy();
-      Stream st = s0;
-      int s = 0;
-      uint32_t ph = 0;
-      for (int q = 0; q < S_tot; ++q, st.advance()) {
-        const bool nul = st.null();
-        const int il = st.item();
-        const int64_t n = blockIdx.x + (int64_t)il * gridDim.x;
-        if (!nul && st.cluster() == 0 && st.j == 0) {  // whole-item Y block
-          const int y = il % NY;
-          if (il >= NY) wc.wait(&y_empty[y], (uint32_t)(((il / NY) - 1) & 1), 1);
-          const uint32_t yb = (uint32_t)T * p.B * 8;
-          mbar_arrive_expect_tx(&y_full[y], yb);
-          bulk_g2s(smem + L.yst + y * L.ybytes, p.Y + (size_t)n * T * p.B, yb, &y_full[y], policy);
+    // stage (group g, row block k): lane 0 arms the barrier, then the copies
+    // are issued from several lanes (one bulk copy costs the issuing thread
+    // a few hundred cycles; a stage is at most 2 + T copies)
+    const uint64_t policy = l2_evict_first_policy();
+    int s = 0;
+    uint32_t ph = 0;
+    int seq = 0;
+    for (int g = 0; g < n_groups; ++g) {
+      const int64_t n0 = first + (int64_t)g * ips;
+      const int cnt = (int)min((int64_t)ips, my_items - (int64_t)g * ips);
+      for (int k = 0; k < spi; ++k, ++seq) {
+        const int r0 = st_row0[k], R = st_rows[k];
+        const uint32_t hb = (uint32_t)cnt * R * p.us * 8, yb = (uint32_t)cnt * T * R * 8;
+        if (lane == 0) {
+          if (seq >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
+          mbar_arrive_expect_tx(&raw_full[s], hb + yb);
         }
-        if (q >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
-        if (nul) {
-          mbar_arrive(&raw_full[s]);  // empty chunk: the converter writes zeros
-        } else {
-          const ChunkDesc cd = p.chunks[st.chunk_index()];
-          const uint32_t hb = (uint32_t)cd.nrows * p.us * 8;
-          mbar_arrive_expect_tx(&raw_full[s], hb);
-          bulk_g2s(smem + L.hst + s * L.hbytes, p.H + ((size_t)n * p.B + cd.row0) * p.us, hb, &raw_full[s],
-                   policy);
+        __syncwarp();
+        char* dst = smem + L.stg + s * L.sbytes;
+        if (spi == 1) {  // whole items: H and Y of `cnt` consecutive items are contiguous
+          if (lane == 0) bulk_g2s(dst, p.H + (size_t)n0 * p.B * p.us, hb, &raw_full[s], policy);
+          if (lane == 1) bulk_g2s(dst + p.stage_hbytes, p.Y + (size_t)n0 * T * p.B, yb, &raw_full[s], policy);
+        } else {  // row block of one item: H rows in one copy, Y one copy per symbol row
+          if (lane == 0) bulk_g2s(dst, p.H + ((size_t)n0 * p.B + r0) * p.us, hb, &raw_full[s], policy);
+          if (lane < T)
+            bulk_g2s(dst + p.stage_hbytes + lane * R * 8, p.Y + ((size_t)n0 * T + lane) * p.B + r0, R * 8,
+                     &raw_full[s], policy);
         }
         if (++s == NS) {
           s = 0;
@@ -398,26 +402,22 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer ----
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_tf32_mn(128, N);
       const uint32_t lbo = (uint32_t)L.lbo;
       const uint32_t ops = smem_u32(smem + L.ops);
-      Stream st = s0;
-      for (int pq = 0; pq < S_tot / pair; ++pq) {  // one tile per (pair v, chunk j)
-        const int b = pq % TC_NOP;
-        const int v = pq / cpu, j = pq - v * cpu;
-        wc.wait(&op_full[b], (uint32_t)((pq / TC_NOP) & 1), 1);
+      int b = 0;
+      uint32_t bph = 0;
+      for (int v = 0, pq = 0; v < n_pairs; ++v)
+        for (int j = 0; j < cpu; ++j, ++pq) {  // one tile per (pair v, chunk j)
+        wc.wait(&op_full[b], bph, 1);
         if (p.dbg_tile && blockIdx.x == 0 && pq == 0) {
           const float* t = reinterpret_cast<const float*>(smem + L.ops);
           for (int e = 0; e < L.opb / 4; ++e) p.dbg_tile[e] = t[e];
         }
-        st.v = v;
-        st.j = j;
-        st.h = 0;
-        const ChunkDesc cd = p.chunks[st.chunk_index()];
+        const ChunkDesc cd = chunks[j];  // units share the chunk structure
         const int a = v & 1;
         if (j == 0 && v >= 2) wc.wait(&acc_empty[a], (uint32_t)(((v >> 1) - 1) & 1), 2);
         tc_fence_after();
@@ -433,8 +433,17 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           umma_tf32(d, ah, al, idesc, 1u);
           umma_tf32(d, al, ah, idesc, 1u);
         }
-        umma_commit(&op_empty[b]);
-        if (j == cpu - 1) umma_commit(&acc_full[a]);
+        if (p.ablate & 16) {  // timing study: plain arrives instead of tcgen05.commit
+          mbar_arrive(&op_empty[b]);
+          if (j == cpu - 1) mbar_arrive(&acc_full[a]);
+        } else {
+          umma_commit(&op_empty[b]);
+          if (j == cpu - 1) umma_commit(&acc_full[a]);
+        }
+        if (++b == TC_NOP) {
+          b = 0;
+          bph ^= 1u;
+        }
       }
     }
     __syncwarp();
@@ -443,16 +452,21 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
     // H rows: one float4 (2 UEs) per task, written to the same antenna row of
     // the tile (4 rows x 8 chunks per warp: one wavefront per row).  Y: task
-    // (symbol pair tp, antenna pair) reads Y[2tp][k..k+1] and Y[2tp+1][k..k+1]
-    // and writes chunk tp of antenna rows k and k+1.  Pad rows/features of
-    // the tiles were zeroed at kernel start and are never written.
+    // (symbol pair tp, antenna pair k) reads Y[2tp][k..k+1], Y[2tp+1][k..k+1]
+    // and writes chunk tp of antenna rows k and k+1; a warp takes 4 symbol
+    // pairs x 8 antenna pairs, so its loads are 4 whole 128-byte row segments
+    // and its stores hit every chunk position of the swizzle 4 times (4
+    // wavefronts, the minimum).  Pad rows/features of the tiles were zeroed at
+    // kernel start and are never written.  Full chunks (KC rows) use per-thread
+    // task offsets computed once; one iteration converts a whole pair-chunk.
     const int ct = tid - 64;
     const int us2 = 2 * p.us;
     const int hq = p.us / 2;             // float4 per stored H row
     constexpr int HQ = UP / 2;           // float4 slots per H row of the tile
+    constexpr int HT = 32 * HQ / TC_CONV;  // H tasks per thread in a full chunk
+    static_assert(HT * TC_CONV == 32 * HQ, "full-chunk H tasks must divide evenly");
     const int lbo = L.lbo;
     const int tpairs = (T + 1) / 2;
-    const int yrow = 2 * p.B;            // floats per Y symbol row
     auto split = [](float x, float& h, float& l) {
       h = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
       l = x - h;
@@ -466,65 +480,159 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       *reinterpret_cast<float4*>(hi + off) = hh;
       *reinterpret_cast<float4*>(lo + off) = ll;
     };
-    Stream st = s0;
-    int s = 0;
-    uint32_t ph = 0;
-    for (int q = 0; q < S_tot; ++q, st.advance()) {
-      const int pq = q / pair;
-      const int b = pq % TC_NOP;
-      const int h = st.h;
-      const bool nul = st.null();
-      const int il = st.item();
-      const int y = il % NY;
-      wc.wait(&raw_full[s], ph, 1);
-      if (!nul) wc.wait(&y_full[y], (uint32_t)((il / NY) & 1), 2);
-      if (h == 0 && pq >= TC_NOP) wc.wait(&op_empty[b], (uint32_t)(((pq / TC_NOP) - 1) & 1), 3);
-      // a null half (odd unit count) is left as is: its rows and columns of
-      // the accumulator are never read, and rows/columns do not mix
-      if (!nul && !(p.ablate & 4)) {
-        const ChunkDesc cd = p.chunks[st.chunk_index()];
-        const int nr = cd.nrows, nr8 = (nr + 7) & ~7;
-        const float* Hf = reinterpret_cast<const float*>(smem + L.hst + s * L.hbytes);
-        const float* Yf = reinterpret_cast<const float*>(smem + L.yst + y * L.ybytes) + 2 * cd.row0;
+    // per-thread task tables of a full chunk (half h adds its own store offsets)
+    int h_ld[HT], h_st[2][HT];
+    bool h_ok[HT];
+#pragma unroll
+    for (int r = 0; r < HT; ++r) {
+      const int e = ct + r * TC_CONV;
+      const int kr = e / HQ, c4 = e % HQ;
+      h_ok[r] = c4 < hq;
+      h_ld[r] = kr * us2 + 4 * c4;
+      h_st[0][r] = mn_off(4 * c4, kr, lbo);
+      h_st[1][r] = mn_off(2 * UP + 4 * c4, kr, lbo);
+    }
+    const int ytp = 4 * ((ct >> 5) >> 1) + ((ct >> 3) & 3);
+    const int yk = 2 * ((ct & 7) + 8 * ((ct >> 5) & 1));
+    const bool y_ok = ytp < tpairs;
+    const bool y_ok1 = 2 * ytp + 1 < T;
+    // Y loads: symbol rows 2tp, 2tp+1 of the staged block (row stride yrow)
+    int y_st[2][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      y_st[h][0] = mn_off(YB + 32 * h + 4 * ytp, yk, lbo);
+      y_st[h][1] = mn_off(YB + 32 * h + 4 * ytp, yk + 1, lbo);
+    }
+    int b = 0;
+    uint32_t bph = 0;
+    // unit cursor: (item, cluster) of the next unit, its slot in the stage
+    // group and the ring position / phase of the group's first stage (no
+    // divisions in the loop: a lone warp pays ~100 cycles per division)
+    int cu_il = 0, cu_c = 0, cu_sl = 0, cu_gpos = 0;
+    uint32_t cu_gph = 0;
+    for (int v = 0; v < n_pairs; ++v) {
+      int il[2], cl[2], sl[2], gpos[2];
+      uint32_t gph[2];
+      bool real[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        il[h] = cu_il;
+        cl[h] = cu_c;
+        sl[h] = cu_sl;
+        gpos[h] = cu_gpos;
+        gph[h] = cu_gph;
+        real[h] = (h < pair) && (v * pair + h < U_tot);
+        if (h < pair && ++cu_c == upi) {
+          cu_c = 0;
+          ++cu_il;
+          if (++cu_sl == ips) {
+            cu_sl = 0;
+            cu_gpos += spi;
+            while (cu_gpos >= NS) {
+              cu_gpos -= NS;
+              cu_gph ^= 1u;
+            }
+          }
+        }
+      }
+      for (int j = 0; j < cpu; ++j) {
+        // wait for the stages of both halves, then for the operand tile
+        int sslot[2], sflags[2];
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= pair) continue;
+          if (!real[h]) continue;
+          sflags[h] = chunks[cl[h] * cpu + j].flags;
+          int pos = gpos[h] + ((sflags[h] >> CH_STAGE_SHIFT) & 0xff);
+          uint32_t sp = gph[h];
+          while (pos >= NS) {
+            pos -= NS;
+            sp ^= 1u;
+          }
+          sslot[h] = pos;
+          wc.wait(&raw_full[pos], sp, 1);
+        }
+        if (v * cpu + j >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
+        const long long t_body = rec ? clock64() : 0;
         char* hi = smem + L.ops + 2 * b * L.opb;
         char* lo = hi + L.opb;
-        const int fh = h * 2 * UP;             // first M row of this unit's H features
-        const int fy = YB + 32 * h;            // first M row of this unit's Y block
-        for (int e = ct; e < nr8 * HQ; e += TC_CONV) {
-          const int kr = e / HQ, c4 = e % HQ;
-          if (c4 >= hq) continue;
-          const float4 v = (kr < nr) ? *reinterpret_cast<const float4*>(Hf + kr * us2 + 4 * c4)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-          put(hi, lo, mn_off(fh + 4 * c4, kr, lbo), v);
-        }
-        // Y tasks: a warp takes 4 symbol pairs x 8 antenna pairs, so its loads
-        // are 4 full 128-byte row segments and its stores hit all 8 chunk
-        // positions of the swizzle 4 times each (4 wavefronts, the minimum)
-        const int kb8 = (nr8 / 2 + 7) / 8;    // 8-antenna-pair blocks
-        const int ntask = 32 * kb8 * ((tpairs + 3) / 4);
-        for (int e = ct; e < ntask; e += TC_CONV) {
-          const int blk = e >> 5;
-          const int tp = 4 * (blk / kb8) + ((e >> 3) & 3);
-          const int k = 2 * ((e & 7) + 8 * (blk % kb8));
-          if (tp >= tpairs || k >= nr8) continue;
-          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-          if (k < nr) {
-            a0 = *reinterpret_cast<const float4*>(Yf + 2 * tp * yrow + 2 * k);
-            if (2 * tp + 1 < T) a1 = *reinterpret_cast<const float4*>(Yf + (2 * tp + 1) * yrow + 2 * k);
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= pair) continue;
+          if (!real[h] || (p.ablate & 4)) continue;  // null half: rows/columns never read
+          const ChunkDesc cd = chunks[cl[h] * cpu + j];
+          const int nr = cd.nrows;
+          const int k = (cd.flags >> CH_STAGE_SHIFT) & 0xff;
+          const int R = st_rows[k], dr = cd.row0 - st_row0[k], slot = sl[h];
+          const char* sb = smem + L.stg + sslot[h] * L.sbytes;
+          const float* Hf = reinterpret_cast<const float*>(sb) + (size_t)(slot * R + dr) * us2;
+          const float* Yf = reinterpret_cast<const float*>(sb + p.stage_hbytes) + (size_t)slot * T * R * 2 + 2 * dr;
+          const int yrow = 2 * R;  // floats per staged Y symbol row
+          if (nr == 32) {
+            float4 hv[HT], ya = make_float4(0.f, 0.f, 0.f, 0.f), yb = ya;
+#pragma unroll
+            for (int r = 0; r < HT; ++r)
+              if (h_ok[r]) hv[r] = *reinterpret_cast<const float4*>(Hf + h_ld[r]);
+            if (y_ok) {
+              ya = *reinterpret_cast<const float4*>(Yf + 2 * ytp * yrow + 2 * yk);
+              if (y_ok1) yb = *reinterpret_cast<const float4*>(Yf + (2 * ytp + 1) * yrow + 2 * yk);
+            }
+#pragma unroll
+            for (int r = 0; r < HT; ++r)
+              if (h_ok[r]) put(hi, lo, h_st[h][r], hv[r]);
+            if (y_ok) {
+              put(hi, lo, y_st[h][0], make_float4(ya.x, ya.y, yb.x, yb.y));
+              put(hi, lo, y_st[h][1], make_float4(ya.z, ya.w, yb.z, yb.w));
+            }
+            continue;
           }
-          const int f = fy + 4 * tp;
-          put(hi, lo, mn_off(f, k, lbo), make_float4(a0.x, a0.y, a1.x, a1.y));
-          put(hi, lo, mn_off(f, k + 1, lbo), make_float4(a0.z, a0.w, a1.z, a1.w));
+          // partial chunk (ragged cluster): generic loops, K rows zero-padded to 8
+          const int nr8 = (nr + 7) & ~7;
+          const int fh = h * 2 * UP;
+          const int fy = YB + 32 * h;
+          for (int e = ct; e < nr8 * HQ; e += TC_CONV) {
+            const int kr = e / HQ, c4 = e % HQ;
+            if (c4 >= hq) continue;
+            const float4 v4 = (kr < nr) ? *reinterpret_cast<const float4*>(Hf + kr * us2 + 4 * c4)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            put(hi, lo, mn_off(fh + 4 * c4, kr, lbo), v4);
+          }
+          const int kb8 = (nr8 / 2 + 7) / 8;
+          const int ntask = 32 * kb8 * ((tpairs + 3) / 4);
+          for (int e = ct; e < ntask; e += TC_CONV) {
+            const int blk = e >> 5;
+            const int tp = 4 * (blk / kb8) + ((e >> 3) & 3);
+            const int k = 2 * ((e & 7) + 8 * (blk % kb8));
+            if (tp >= tpairs || k >= nr8) continue;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+            if (k < nr) {
+              a0 = *reinterpret_cast<const float4*>(Yf + 2 * tp * yrow + 2 * k);
+              if (2 * tp + 1 < T) a1 = *reinterpret_cast<const float4*>(Yf + (2 * tp + 1) * yrow + 2 * k);
+            }
+            const int f = fy + 4 * tp;
+            put(hi, lo, mn_off(f, k, lbo), make_float4(a0.x, a0.y, a1.x, a1.y));
+            put(hi, lo, mn_off(f, k + 1, lbo), make_float4(a0.z, a0.w, a1.z, a1.w));
+          }
+        }
+        const long long t_fence = rec ? clock64() : 0;
+        if (rec) cnt[2] += t_fence - t_body;
+        fence_proxy_async_smem();
+        mbar_arrive(&op_full[b]);
+        if (rec) cnt[3] += clock64() - t_fence;
+        // release a stage after the last chunk that reads it (host-computed
+        // per item; a multi-item stage after its last item)
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= pair) continue;
+          if (!real[h] || !(sflags[h] & CH_STAGE_REL)) continue;
+          if (spi == 1 && sl[h] != ips - 1 && il[h] != my_items - 1) continue;
+          mbar_arrive(&raw_empty[sslot[h]]);
+        }
+        if (++b == TC_NOP) {
+          b = 0;
+          bph ^= 1u;
         }
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&op_full[b]);
-      mbar_arrive(&raw_empty[s]);
-      if (++s == NS) {
-        s = 0;
-        ph ^= 1u;
-      }
-      if (!nul && st.cluster() == upi - 1 && st.j == cpu - 1) mbar_arrive(&y_empty[y]);  // item converted
     }
   } else if (warp < TC_FIRST_SOLVER) {
     // -------------------------------------------------------- assemblers ----
@@ -536,19 +644,35 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const int hh = is_h ? m / (2 * UP) : (m - YB) / 32;
     const bool has_row = is_h || (m >= YB && m < MU && ((m - YB) & 31) < 2 * T);
     const bool warp_rows = 32 * wq < MU;
+    int ssl = 0;  // solver slot of unit v * pair (round robin, no divisions)
+    uint32_t sph = 0;
     for (int v = 0; v < n_pairs; ++v) {
       const int a = v & 1;
+      int slot[2];
+      uint32_t sphase[2];
+      #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h >= pair) continue;
+        slot[h] = ssl;
+        sphase[h] = sph;
+        if (++ssl == nsolv) {
+          ssl = 0;
+          sph ^= 1u;
+        }
+      }
       // both halves' solver slots must be free before writing either
-      for (int h = 0; h < pair; ++h) {
+      #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h >= pair) continue;
         const int u = v * pair + h;
-        if (u < U_tot && u >= nsolv) wc.wait(&slot_empty[u % nsolv], (uint32_t)(((u / nsolv) - 1) & 1), 1);
+        if (u < U_tot && u >= nsolv) wc.wait(&slot_empty[slot[h]], sphase[h] ^ 1u, 1);
       }
       wc.wait(&acc_full[a], (uint32_t)((v >> 1) & 1), 2);
       tc_fence_after();
       const int u_mine = v * pair + hh;
       if (warp_rows) {
         const bool write = has_row && u_mine < U_tot;
-        const Work w = work_at(smem, L, u_mine % nsolv, UP);
+        const Work w = work_at(smem, L, hh ? slot[1] : slot[0], UP);
         float* Gf = reinterpret_cast<float*>(w.G);
         float* Zf = reinterpret_cast<float*>(w.Z);
         const int LD = w.LD;
@@ -581,9 +705,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[a]);
-      for (int h = 0; h < pair; ++h) {
+      #pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h >= pair) continue;
         const int u = v * pair + h;
-        if (u < U_tot) mbar_arrive(&slot_full[u % nsolv]);
+        if (u < U_tot) mbar_arrive(&slot_full[slot[h]]);
       }
     }
   } else {
@@ -592,11 +718,16 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const Team<32, -1> tm{lane};
     const Work w = work_at(smem, L, sv, UP);
     int cl_first = 1;
-    for (int u = sv; u < U_tot; u += nsolv) {
-      const int il = u / upi, c = u % upi;
-      const int64_t n = blockIdx.x + (int64_t)il * gridDim.x;
+    int il = 0, c = sv;  // (item, cluster) of unit u, advanced without divisions
+    while (c >= upi) {
+      c -= upi;
+      ++il;
+    }
+    uint32_t ph = 0;
+    for (int u = sv; u < U_tot; u += nsolv, ph ^= 1u) {
+      const int64_t n = first + il;
       const bool item_end = (c == upi - 1);
-      wc.wait(&slot_full[sv], (uint32_t)((u / nsolv) & 1), 1);
+      wc.wait(&slot_full[sv], ph, 1);
       reset_flags(w, tm);
       tm.sync();
       if (p.ablate & 1) {
@@ -623,11 +754,16 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       }
       tm.sync();
       if (lane == 0) mbar_arrive(&slot_empty[sv]);
+      c += nsolv;
+      while (c >= upi) {
+        c -= upi;
+        ++il;
+      }
     }
   }
   if (rec) {
     cnt[0] = clock64() - t_start;
-    for (int k = 0; k < 4; ++k) atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg + role * 4 + k),
+    for (int k = 0; k < 4; ++k) atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg + warp * 4 + k),
                                           (unsigned long long)cnt[k]);
   }
   tc_fence_before();
