@@ -49,7 +49,7 @@ struct EqParams {
   int pair;        // tensor-core kernel: units per operand tile (1 or 2)
   // tensor-core kernel staging: a stage is `ips` consecutive whole items
   // (spi == 1) or one row block of one item (spi > 1); H part then Y part
-  int ips, spi, stage_bytes, stage_hbytes;
+  int ips, spi, stage_bytes, stage_hbytes, stage_ystride;
   int st_row0[MAX_SPI], st_rows[MAX_SPI];
   float* dbg_tile;  // debug: first operand tile of CTA 0 (DBP_TC_DUMP)
   long long* dbg;  // debug: per-role wait-cycle counters [5][4] (DBP_TC_DEBUG)

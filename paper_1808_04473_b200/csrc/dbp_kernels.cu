@@ -260,7 +260,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     for (int j = 0; j < p.nchunks; ++j) {
       const ChunkDesc& cd = p.chunks[j];
       const bool boundary = (cd.row0 == p.chunks[(cd.cluster / unit_step) * unit_step * cpu].row0) || !per_cluster;
-      if (rows > 0 && boundary && (rows + cd.nrows) * (hrow + yrow) > smax) {
+      if (rows > 0 && boundary && (rows + cd.nrows) * (hrow + yrow) + 16 * p.T > smax) {
         if (p.spi == MAX_SPI) return 1;
         p.st_row0[p.spi] = r0;
         p.st_rows[p.spi++] = rows;
@@ -275,8 +275,12 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   }
   int rmax = 0;
   for (int k = 0; k < p.spi; ++k) rmax = std::max(rmax, p.st_rows[k]);
+  // Y symbol rows are staged with a 16-byte pad (row stride = 65 16-byte
+  // chunks for 128 antennas) so that the converter's transposing loads of
+  // symbols 2tp, 2tp+1 spread over all banks
   p.stage_hbytes = p.ips * rmax * hrow;
-  p.stage_bytes = p.stage_hbytes + p.ips * rmax * yrow;
+  p.stage_ystride = rmax * 8 + 16;
+  p.stage_bytes = p.stage_hbytes + p.ips * p.T * p.stage_ystride;
   // chunk -> stage, and the last chunk of the item's visit order touching
   // each stage (units of an item in order; paired clusters interleave)
   for (int j = 0; j < p.nchunks; ++j) {

@@ -380,22 +380,24 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       const int cnt = (int)min((int64_t)ips, my_items - (int64_t)g * ips);
       for (int k = 0; k < spi; ++k, ++seq) {
         const int r0 = st_row0[k], R = st_rows[k];
-        const uint32_t hb = (uint32_t)cnt * R * p.us * 8, yb = (uint32_t)cnt * T * R * 8;
+        const uint32_t hb = (uint32_t)cnt * R * p.us * 8, yb = (uint32_t)cnt * T * R * 8;  // bytes landing
         if (lane == 0) {
           if (seq >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
           mbar_arrive_expect_tx(&raw_full[s], hb + yb);
         }
         __syncwarp();
         char* dst = smem + L.stg + s * L.sbytes;
-        if (spi == 1) {  // whole items: H and Y of `cnt` consecutive items are contiguous
+        // H rows of the `cnt` items: one copy when whole items are staged
+        // (consecutive items are contiguous), else one per item; Y: one copy
+        // per (item, symbol) row into the padded row layout, spread over lanes
+        if (spi == 1) {
           if (lane == 0) bulk_g2s(dst, p.H + (size_t)n0 * p.B * p.us, hb, &raw_full[s], policy);
-          if (lane == 1) bulk_g2s(dst + p.stage_hbytes, p.Y + (size_t)n0 * T * p.B, yb, &raw_full[s], policy);
-        } else {  // row block of one item: H rows in one copy, Y one copy per symbol row
-          if (lane == 0) bulk_g2s(dst, p.H + ((size_t)n0 * p.B + r0) * p.us, hb, &raw_full[s], policy);
-          if (lane < T)
-            bulk_g2s(dst + p.stage_hbytes + lane * R * 8, p.Y + ((size_t)n0 * T + lane) * p.B + r0, R * 8,
-                     &raw_full[s], policy);
+        } else if (lane == 0) {
+          bulk_g2s(dst, p.H + ((size_t)n0 * p.B + r0) * p.us, hb, &raw_full[s], policy);
         }
+        for (int r = lane; r < cnt * T; r += 32)
+          bulk_g2s(dst + p.stage_hbytes + r * p.stage_ystride, p.Y + ((size_t)n0 * T + r) * p.B + r0, R * 8,
+                   &raw_full[s], policy);
         if (++s == NS) {
           s = 0;
           ph ^= 1u;
@@ -492,8 +494,12 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       h_st[0][r] = mn_off(4 * c4, kr, lbo);
       h_st[1][r] = mn_off(2 * UP + 4 * c4, kr, lbo);
     }
-    const int ytp = 4 * ((ct >> 5) >> 1) + ((ct >> 3) & 3);
-    const int yk = 2 * ((ct & 7) + 8 * ((ct >> 5) & 1));
+    // Y task of a full chunk: 8 symbol pairs x 16 antenna pairs over the 128
+    // converter threads; a quarter-warp takes 4 symbol pairs x 2 antenna
+    // pairs, so its 16-byte loads (padded staged rows) and its stores (the
+    // operand swizzle) each hit 8 distinct bank groups
+    const int ytp = (ct & 3) + 4 * ((ct >> 5) & 1);
+    const int yk = 2 * (((ct >> 2) & 1) + 2 * ((ct >> 3) & 3) + 8 * (ct >> 6));
     const bool y_ok = ytp < tpairs;
     const bool y_ok1 = 2 * ytp + 1 < T;
     // Y loads: symbol rows 2tp, 2tp+1 of the staged block (row stride yrow)
@@ -566,8 +572,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           const int R = st_rows[k], dr = cd.row0 - st_row0[k], slot = sl[h];
           const char* sb = smem + L.stg + sslot[h] * L.sbytes;
           const float* Hf = reinterpret_cast<const float*>(sb) + (size_t)(slot * R + dr) * us2;
-          const float* Yf = reinterpret_cast<const float*>(sb + p.stage_hbytes) + (size_t)slot * T * R * 2 + 2 * dr;
-          const int yrow = 2 * R;  // floats per staged Y symbol row
+          const float* Yf =
+              reinterpret_cast<const float*>(sb + p.stage_hbytes + (size_t)slot * T * p.stage_ystride) + 2 * dr;
+          const int yrow = p.stage_ystride / 4;  // floats per staged Y symbol row
           if (nr == 32) {
             float4 hv[HT], ya = make_float4(0.f, 0.f, 0.f, 0.f), yb = ya;
 #pragma unroll
