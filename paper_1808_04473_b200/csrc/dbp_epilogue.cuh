@@ -132,17 +132,24 @@ __device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, in
   }
   const float tolf = 8.f * (float)u * FLT_EPSILON;
   bool bad = false;
+  // the pivot loop stays rolled (a small instruction footprint for the
+  // warp-specialized kernel); the pivot row's register is picked by selects,
+  // never by a dynamic register index.  Padded steps k >= u are no-ops.
+#pragma unroll 1
+  for (int k = 0; k < u; ++k) {
+    const int kr = k / RS, own = (k % RS) * UP + k;  // lane holding (k, k) in register kr
+    float2 mk = m[0];
 #pragma unroll
-  for (int k = 0; k < UP; ++k) {
-    const int own = (k % RS) * UP + k;  // lane holding (k, k) in register k / RS
-    float p = __shfl_sync(0xffffffffu, m[k / RS].x, own);
+    for (int r = 1; r < EPT; ++r)
+      if (r == kr) mk = m[r];
+    float p = __shfl_sync(0xffffffffu, mk.x, own);
     const float d0 = __shfl_sync(0xffffffffu, dgl, own);
-    if (k < u && !(p > tolf * d0)) {
+    if (!(p > tolf * d0)) {
       bad = true;
       p = 1.f;
     }
     const float rp = 1.f / p;
-    const float2 rkj = shfl2(m[k / RS], (k % RS) * UP + j);
+    const float2 rkj = shfl2(mk, (k % RS) * UP + j);
     const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
@@ -174,16 +181,16 @@ __device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, in
     const float sc = unb ? 1.f / cgain : 1.f;
     for (int t = rb; t < T; t += RS) {
       const float2* zr = w.Z + t * LD;
-      float2 acc = make_float2(0.f, 0.f);
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;  // two independent chains
 #pragma unroll
       for (int c = 0; c < UP; c += 2) {
         if (c < u) {
           const float4 v = *reinterpret_cast<const float4*>(zr + c);
-          c_fma(acc, arow[c], make_float2(v.x, v.y));
-          if (c + 1 < u) c_fma(acc, arow[c + 1], make_float2(v.z, v.w));
+          c_fma(acc0, arow[c], make_float2(v.x, v.y));
+          if (c + 1 < u) c_fma(acc1, arow[c + 1], make_float2(v.z, v.w));
         }
       }
-      w.X[t * LD + i] = c_scale(acc, sc);
+      w.X[t * LD + i] = c_scale(c_add(acc0, acc1), sc);
     }
     if (rb == 0) {
       if (a.kind == EQ_ZF) {
@@ -449,13 +456,16 @@ __device__ __forceinline__ void write_status(const Work& w, const EqParams& p, i
 // team is synchronised).  PD: equalize + outputs; FD: equalize one cluster +
 // fold into the fusion sums, finalize on the item's last cluster; STATS:
 // write {G, y_mrc}.  Ends with a team barrier.
-template <int UP, class TM>
+// CLS: equalizer class known at compile time (0 stats only, 1 linear, 2 LAMA)
+// so a kernel instantiated for one class carries no code of the others; -1
+// decides at run time (SIMT kernels).
+template <int UP, class TM, int CLS = -1>
 __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int cluster, bool item_end,
-                              int& cl_first, const TM& tm) {
+                              int& cl_first, const TM& tm, long long* dbg_solve = nullptr) {
   constexpr int NT = TM::N;
   const int tid = tm.t;
   const int u = p.u, T = p.T, LD = w.LD;
-  if (p.arch == ARCH_STATS) {
+  if (CLS == 0 || (CLS < 0 && p.arch == ARCH_STATS)) {
     const int ncl = p.sum_clusters ? 1 : p.C;
     const int cl = p.sum_clusters ? 0 : cluster;
     float2* dst = p.stats_out + ((size_t)n * ncl + cl) * (size_t)(u * u + T * u);
@@ -465,7 +475,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
     return;
   }
   const float n0 = item_n0(p, n);
-  const bool lama = p.kind == EQ_LAMA;
+  const bool lama = CLS == 2 || (CLS < 0 && p.kind == EQ_LAMA);
   EpiArgs a;
   a.kind = p.kind;
   a.u = u;
@@ -490,14 +500,26 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
       }
       lama_unit(w, a, p.cp, tz, ts, tv, tp, tm);
     } else {
+      const long long t0 = dbg_solve ? clock64() : 0;
       linear_unit<UP>(w, a, tm);
+      if (dbg_solve) *dbg_solve += clock64() - t0;
     }
-    for (int e = tid; e < T * u; e += NT) {
-      const int t = e / u, i = e - t * u;
-      const float2 x = w.X[t * LD + i];
-      const size_t o = ((size_t)n * T + t) * u + i;
-      p.xhat[o] = x;
-      if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+    if (u == UP) {  // shifts instead of divisions
+      for (int e = tid; e < T * UP; e += NT) {
+        const int t = e / UP, i = e % UP;
+        const float2 x = w.X[t * LD + i];
+        const size_t o = (size_t)n * T * UP + e;
+        p.xhat[o] = x;
+        if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+      }
+    } else {
+      for (int e = tid; e < T * u; e += NT) {
+        const int t = e / u, i = e - t * u;
+        const float2 x = w.X[t * LD + i];
+        const size_t o = ((size_t)n * T + t) * u + i;
+        p.xhat[o] = x;
+        if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+      }
     }
     if (lama) {
       for (int t = tid; t < T; t += NT) p.sigma2[(size_t)n * T + t] = w.s2[t];

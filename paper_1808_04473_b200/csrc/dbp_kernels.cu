@@ -315,7 +315,10 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   while (nsolv > 2 && !fits(p.NS, nsolv)) --nsolv;
   const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, p.NS, p.C, lama, fd, nsolv);
   if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
-  auto kern = tc_kernel<UP>;
+  const bool fdm = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
+  auto kern = (p.arch == ARCH_STATS) ? tc_kernel<UP, TC_STATS>
+              : fdm ? (lama ? tc_kernel<UP, TC_FD_LAMA> : tc_kernel<UP, TC_FD_LIN>)
+                    : (lama ? tc_kernel<UP, TC_PD_LAMA> : tc_kernel<UP, TC_PD_LIN>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int threads = 32 * (TC_FIRST_SOLVER + nsolv);

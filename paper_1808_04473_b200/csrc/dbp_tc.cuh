@@ -277,7 +277,11 @@ struct Stream {
   __device__ __forceinline__ int chunk_index() const { return cluster() * cpu + j; }
 };
 
-template <int UP>
+// MODE: what the unit epilogue does, fixed per instantiation so that each
+// kernel carries only its own epilogue code (instruction-cache footprint)
+enum { TC_STATS = 0, TC_PD_LIN = 1, TC_PD_LAMA = 2, TC_FD_LIN = 3, TC_FD_LAMA = 4 };
+
+template <int UP, int MODE>
 __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv) {
   extern __shared__ __align__(1024) char smem[];
   const int pair = p.pair;
@@ -285,9 +289,13 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   constexpr int SW = 2 * 2 * UP;  // TMEM columns per accumulator slot (room for pair == 2)
   constexpr uint32_t TMEM_COLS = (2 * SW <= 32) ? 32 : (2 * SW <= 64) ? 64 : (2 * SW <= 128) ? 128
                                  : (2 * SW <= 256) ? 256 : 512;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool lama = p.kind == EQ_LAMA;
-  const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
+  // warp index broadcast from lane 0: the compiler then treats the role
+  // branches as warp-uniform, so shuffles inside them compile to plain SHFL
+  // instead of divergence-safe COLLECTIVE sequences
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  constexpr bool lama = (MODE == TC_PD_LAMA || MODE == TC_FD_LAMA);
+  constexpr bool fd = (MODE == TC_FD_LIN || MODE == TC_FD_LAMA);
+  constexpr int CLS = (MODE == TC_STATS) ? 0 : lama ? 2 : 1;
   const int NS = p.NS;
   const int T = p.T;
   const int HR = pair * 2 * UP;          // H rows of the tile (= MMA N)
@@ -739,7 +747,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       tm.sync();
       if (p.ablate & 1) {
       } else if (!fd) {
-        unit_epilogue<UP>(w, p, n, c, item_end, cl_first, tm);
+        const long long t0 = rec ? clock64() : 0;
+        unit_epilogue<UP, Team<32, -1>, CLS>(w, p, n, c, item_end, cl_first, tm, rec ? cnt + 2 : nullptr);
+        if (rec) cnt[3] += clock64() - t0;
       } else {
         EpiArgs a;
         a.kind = p.kind;
@@ -752,7 +762,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         a.beta = p.cl_beta[c];
         a.lama_scale = p.cl_scale[c];
         a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
-        if (lama)
+        if constexpr (lama)
           lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
         else
           linear_unit<UP>(w, a, tm);
