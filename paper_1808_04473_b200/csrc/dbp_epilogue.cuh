@@ -44,6 +44,7 @@ struct EqParams {
   float2* stats_out;
   float* fd_acc;
   float* fd_wraw;
+  float* fd_scratch;  // tensor-core FD: per-(item, cluster) records for the ordered fold
   float2 *tr_z, *tr_s, *tr_v;
   float* tr_phi;
   int pair;        // tensor-core kernel: units per operand tile (1 or 2)

@@ -214,6 +214,37 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
   return cuda_check("stream_kernel");
 }
 
+// Per-stream device scratch (FD fold records), grown on demand.  Launches on
+// one stream are ordered, so they may share it; other streams get their own.
+static void* stream_scratch(cudaStream_t st, size_t need) {
+  struct Entry {
+    cudaStream_t st;
+    void* ptr;
+    size_t bytes;
+  };
+  static Entry tab[16];
+  static int used = 0;
+  Entry* e = nullptr;
+  for (int i = 0; i < used; ++i)
+    if (tab[i].st == st) e = &tab[i];
+  if (!e) {
+    if (used == 16) return nullptr;
+    e = &tab[used++];
+    *e = Entry{st, nullptr, 0};
+  }
+  if (need > e->bytes) {
+    if (e->ptr) {
+      cudaStreamSynchronize(st);  // the previous buffer may still be in use on this stream
+      cudaFree(e->ptr);
+    }
+    e->ptr = nullptr;
+    e->bytes = 0;
+    if (cudaMalloc(&e->ptr, need) != cudaSuccess) return nullptr;
+    e->bytes = need;
+  }
+  return e->ptr;
+}
+
 template <int UP>
 static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
@@ -243,11 +274,11 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   const int item_bytes = p.B * (hrow + yrow);
   int smax = 64 * 1024;
   if (const char* e = getenv("DBP_TC_SMAX")) smax = atoi(e) * 1024;
-  if (p.pair == 2 && upi == 1 && 2 * item_bytes > smax) p.pair = 1;  // item pairs must share a stage
-  const int step = (p.pair == 2 && upi == 1) ? 2 : 1;
+  // (paired items may sit in different stages: the converter waits for both,
+  // and the ring keeps at least 2 stages, all filled in order)
   if (item_bytes <= smax) {
     p.spi = 1;
-    p.ips = std::max(step, (smax / item_bytes) / step * step);
+    p.ips = std::max(1, smax / item_bytes);
     p.st_row0[0] = 0;
     p.st_rows[0] = p.B;
   } else {
@@ -315,6 +346,11 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   while (nsolv > 2 && !fits(p.NS, nsolv)) --nsolv;
   const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, p.NS, p.C, lama, fd, nsolv);
   if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
+  if (fd) {  // per-(item, cluster) fold records: L2-resident scratch, one per stream, grown on demand
+    const size_t need = (size_t)p.n_items * p.C * fd_record_floats(p.u, p.T, lama ? p.T : p.u) * sizeof(float);
+    p.fd_scratch = static_cast<float*>(stream_scratch(st, need));
+    if (!p.fd_scratch) return fail(DBP_E_CUDA, "FD scratch allocation failed");
+  }
   const bool fdm = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   auto kern = (p.arch == ARCH_STATS) ? tc_kernel<UP, TC_STATS>
               : fdm ? (lama ? tc_kernel<UP, TC_FD_LAMA> : tc_kernel<UP, TC_FD_LIN>)

@@ -49,6 +49,7 @@ constexpr int TC_NOP = 2;  // operand tile ring depth (converter -> MMA)
 constexpr int TC_CONV = 32 * TC_CONV_W;
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
+constexpr int FD_CNT = 64;  // FD arrival counters per CTA (items in flight in the solver stage)
 
 // byte offset of (M row f, antenna kr) in an operand tile: MN-major tf32
 // (128-byte rows, 32-byte granules swizzled by kr % 4; umma_desc_mn_sw128),
@@ -60,31 +61,8 @@ __device__ __forceinline__ int mn_off(int f, int kr, int lbo) {
 // first M row of the Y blocks
 __host__ __device__ constexpr int tc_yrow0(int UP, int pair) { return ((pair * 2 * UP + 31) / 32) * 32; }
 
-// FD item ring slot: the fusion sums of one item, folded cluster by cluster.
-struct ItemSlotLayout {
-  int num, den, harm, wbuf, flags, total;
-};
-
-__host__ __device__ inline ItemSlotLayout make_item_slot(int UP, int TP, int C) {
-  ItemSlotLayout S;
-  const int LD = UP + 2, V = (UP > TP ? UP : TP);
-  int o = 0;
-  S.num = o;
-  o += TP * LD * 8;
-  S.den = o;
-  o += V * 4;
-  S.harm = o;
-  o += V * 4;
-  S.wbuf = o;
-  o += C * V * 4;
-  S.flags = o;
-  o += 16;  // [0] status, [1] divergence iteration, [2] turn counter
-  S.total = align_up(o, 128);
-  return S;
-}
-
 struct TcLayout {
-  int bars, tmem_slot, chunks, stg, sbytes, ops, opb, lbo, work, work_stride, items, item_stride, nir, total;
+  int bars, tmem_slot, chunks, stg, sbytes, ops, opb, lbo, work, work_stride, items, total;
   WorkLayout w;  // offsets relative to a solver's work base
 };
 
@@ -114,11 +92,8 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int sbytes, i
   L.w = make_work_layout(0, UP, TP, C, lama, false);
   L.work_stride = L.w.total;
   o += nsolv * L.work_stride;
-  L.items = o;
-  const ItemSlotLayout S = make_item_slot(UP, TP, C);
-  L.item_stride = S.total;
-  L.nir = fd ? (nsolv + C - 1) / C + 2 : 0;
-  o += L.nir * L.item_stride;
+  L.items = o;  // FD: per-item arrival counters (ring of FD_CNT)
+  o += fd ? FD_CNT * 4 : 0;
   L.total = align_up(o, 128);
   return L;
 }
@@ -147,93 +122,113 @@ __device__ __forceinline__ Work work_at(char* smem, const TcLayout& L, int sv, i
   return make_work(smem, wl, UP);
 }
 
-// FD: fold one solved cluster into its item's ring slot, strictly in cluster
-// order (deterministic sums; a solver waits for its turn), and finalize the
-// item on its last cluster (fusion.py:141-154).  Runs on one warp.
-template <int UP, class TM>
-__device__ void fd_fold(const Work& w, char* slot, const ItemSlotLayout& S, const EqParams& p, int64_t n, int il,
-                        int c, int nir, const TM& tm) {
+// FD fusion without waiting (fusion.py:141-154).  Every solved cluster is
+// stashed as a record {unbiased z_c [T][u], sigma2_c [wdim], MRC gain [u],
+// status, divergence iteration} in an L2-resident scratch array; the solver
+// that brings the item's arrival count to C then folds the C records in
+// cluster order (the reference's summation order: deterministic results) and
+// writes the outputs.  No solver ever waits for another one.
+__host__ __device__ inline int fd_record_floats(int u, int T, int wdim) {
+  return align_up(2 * T * u + wdim + u + 2, 4);
+}
+
+template <class TM>
+__device__ void fd_stash(const Work& w, const EqParams& p, int64_t n, int c, const TM& tm) {
   const int u = p.u, T = p.T, LD = w.LD, C = p.C;
-  const bool lama = p.kind == EQ_LAMA;
-  const int wdim = lama ? T : u;
-  float2* num = reinterpret_cast<float2*>(slot + S.num);
-  float* den = reinterpret_cast<float*>(slot + S.den);
-  float* harm = reinterpret_cast<float*>(slot + S.harm);
-  float* wbuf = reinterpret_cast<float*>(slot + S.wbuf);
-  int* flags = reinterpret_cast<int*>(slot + S.flags);
-  volatile int* turn = flags + 2;
-  const int key = il * C + c;
+  const int wdim = (p.kind == EQ_LAMA) ? T : u;
+  float* rec = p.fd_scratch + ((size_t)n * C + c) * fd_record_floats(u, T, wdim);
+  float2* z = reinterpret_cast<float2*>(rec);
+  for (int e = tm.t; e < T * u; e += TM::N) {
+    const int t = e / u, i = e - t * u;
+    z[e] = w.X[t * LD + i];
+  }
+  for (int e = tm.t; e < wdim; e += TM::N) rec[2 * T * u + e] = w.s2[e];
+  if (p.kind == EQ_MRC)
+    for (int e = tm.t; e < u; e += TM::N) rec[2 * T * u + wdim + e] = w.gn[e];
   if (tm.t == 0) {
-    while (*turn != key) __nanosleep(32);
+    int* f = reinterpret_cast<int*>(rec + 2 * T * u + wdim + u);
+    f[0] = w.flags[0];
+    f[1] = w.flags[1];
+  }
+}
+
+// Ordered fold of the item's C records by one warp.  scratch: >= (C + 1) *
+// wdim floats of the solver's shared memory.
+template <class TM>
+__device__ void fd_finish(float* scratch, const EqParams& p, int64_t n, const TM& tm) {
+  const int u = p.u, T = p.T, C = p.C;
+  const bool lama = p.kind == EQ_LAMA, mrc = p.kind == EQ_MRC;
+  const int wdim = lama ? T : u;
+  const int rf = fd_record_floats(u, T, wdim);
+  const float* recs = p.fd_scratch + (size_t)n * C * rf;
+  float* den = scratch;         // [wdim]
+  float* wts = scratch + wdim;  // [C][wdim]
+  int st = 0, it = 0x7fffffff;
+  for (int e = tm.t; e < wdim; e += TM::N) {
+    float dsum = 0.f, hsum = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float* rec = recs + (size_t)c * rf;
+      const float s2 = __ldcg(rec + 2 * T * u + e);
+      if (!mrc && !(s2 > 0.f)) st = ST_BADVAR;  // optimal_fusion_weights rejects sigma2 <= 0
+      const float inv = 1.f / fmaxf(s2, VAR_FLOOR);
+      const float wt = mrc ? __ldcg(rec + 2 * T * u + wdim + e) : inv;
+      wts[c * wdim + e] = wt;
+      dsum += wt;
+      hsum += inv;
+    }
+    den[e] = dsum;
+    if (p.arch == ARCH_FD) {
+      p.sigma2[(size_t)n * wdim + e] = 1.f / hsum;
+    } else {
+      float* dst = p.fd_acc + (size_t)n * (2 * T * u + 2 * wdim);
+      dst[2 * T * u + e] = dsum;
+      dst[2 * T * u + wdim + e] = hsum;
+    }
   }
   tm.sync();
-  __threadfence_block();
-  const bool first = (c == 0);
-  for (int e = tm.t; e < wdim; e += TM::N) {
-    const float s2 = w.s2[e];
-    if (p.kind != EQ_MRC && !(s2 > 0.f)) set_status(w.flags, ST_BADVAR);
-    const float inv = 1.f / fmaxf(s2, VAR_FLOOR);
-    const float wt = (p.kind == EQ_MRC) ? w.gn[e] : inv;
-    wbuf[c * wdim + e] = wt;
-    den[e] = first ? wt : den[e] + wt;
-    harm[e] = first ? inv : harm[e] + inv;
+  if (p.arch == ARCH_FD) {
+    if (p.nu)
+      for (int e = tm.t; e < C * wdim; e += TM::N) p.nu[(size_t)n * C * wdim + e] = wts[e] / den[e % wdim];
+  } else {
+    for (int e = tm.t; e < C * wdim; e += TM::N) p.fd_wraw[(size_t)n * C * wdim + e] = wts[e];
   }
   for (int e = tm.t; e < T * u; e += TM::N) {
     const int t = e / u, i = e - t * u;
     const int k = lama ? t : i;
-    const float s2 = w.s2[k];
-    const float wt = (p.kind == EQ_MRC) ? w.gn[k] : 1.f / fmaxf(s2, VAR_FLOOR);
-    const float2 x = c_scale(w.X[t * LD + i], wt);
-    num[t * LD + i] = first ? x : c_add(num[t * LD + i], x);
-  }
-  tm.sync();
-  if (tm.t == 0) {
-    if (first) {
-      flags[0] = 0;
-      flags[1] = 0x7fffffff;
+    float2 num = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) {
+      const float2 zc = __ldcg(reinterpret_cast<const float2*>(recs + (size_t)c * rf) + e);
+      num = c_add(num, c_scale(zc, wts[c * wdim + k]));
     }
-    if (w.flags[0] && flags[0] == 0) flags[0] = w.flags[0];
-    if (w.flags[1] < flags[1]) flags[1] = w.flags[1];
-  }
-  if (c == C - 1) {
-    tm.sync();
-    __threadfence_block();
     if (p.arch == ARCH_FD) {
-      for (int e = tm.t; e < T * u; e += TM::N) {
-        const int t = e / u, i = e - t * u;
-        const float2 x = c_scale(num[t * LD + i], 1.f / den[lama ? t : i]);
-        const size_t o = ((size_t)n * T + t) * u + i;
-        p.xhat[o] = x;
-        if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
-      }
-      for (int e = tm.t; e < wdim; e += TM::N) p.sigma2[(size_t)n * wdim + e] = 1.f / harm[e];
-      if (p.nu)
-        for (int e = tm.t; e < C * wdim; e += TM::N) p.nu[(size_t)n * C * wdim + e] = wbuf[e] / den[e % wdim];
-    } else {  // FD_PARTIAL: raw sums for a cross-GPU reduction
-      const int rec = 2 * T * u + 2 * wdim;
-      float* dst = p.fd_acc + (size_t)n * rec;
-      for (int e = tm.t; e < T * u; e += TM::N) {
-        const int t = e / u, i = e - t * u;
-        const float2 v = num[t * LD + i];
-        dst[2 * e] = v.x;
-        dst[2 * e + 1] = v.y;
-      }
-      for (int e = tm.t; e < wdim; e += TM::N) {
-        dst[2 * T * u + e] = den[e];
-        dst[2 * T * u + wdim + e] = harm[e];
-      }
-      for (int e = tm.t; e < C * wdim; e += TM::N) p.fd_wraw[(size_t)n * C * wdim + e] = wbuf[e];
-    }
-    if (tm.t == 0) {
-      int st = flags[0];
-      if (flags[1] < 0x7fffffff) st = st ? st : ST_DIVERGED;
-      p.status[n] = st;
-      if (p.iters) p.iters[n] = (flags[1] < 0x7fffffff) ? flags[1] : 0;
+      const float2 x = c_scale(num, 1.f / den[k]);
+      const size_t o = (size_t)n * T * u + e;
+      p.xhat[o] = x;
+      if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, p.cp);
+    } else {
+      float* dst = p.fd_acc + (size_t)n * (2 * T * u + 2 * wdim);
+      dst[2 * e] = num.x;
+      dst[2 * e + 1] = num.y;
     }
   }
+  // status: first failing cluster's code, else divergence (earliest iteration)
+  for (int c = 0; c < C; ++c) {
+    const int* f = reinterpret_cast<const int*>(recs + (size_t)c * rf + 2 * T * u + wdim + u);
+    const int fs = __ldcg(f), fi = __ldcg(f + 1);
+    if (st == 0 && fs) st = fs;
+    if (fi < it) it = fi;
+  }
+  // combine the lanes' variance checks
+  for (int o = 16; o > 0; o >>= 1) {
+    const int so = __shfl_xor_sync(0xffffffffu, st, o);
+    if (st == 0) st = so;
+  }
+  if (tm.t == 0) {
+    if (it < 0x7fffffff && st == 0) st = ST_DIVERGED;
+    p.status[n] = st;
+    if (p.iters) p.iters[n] = (it < 0x7fffffff) ? it : 0;
+  }
   tm.sync();
-  __threadfence_block();
-  if (tm.t == 0) *turn = (c == C - 1) ? (il + nir) * C : key + 1;
 }
 
 // Debug instrumentation (p.dbg != nullptr, set by DBP_TC_DEBUG): per-CTA
@@ -302,7 +297,6 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const int YB = tc_yrow0(UP, pair);     // first Y row (32-aligned)
   const int MU = YB + pair * 32;         // rows in use
   const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, NS, p.C, lama, fd, nsolv);
-  const ItemSlotLayout IS = make_item_slot(UP, p.TP, p.C);
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(smem + L.bars);  // stage ring
   uint64_t* raw_empty = raw_full + NS;
   uint64_t* op_full = raw_empty + NS;
@@ -340,12 +334,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     }
     fence_mbar_init();
   }
-  for (int k = tid; k < L.nir; k += blockDim.x) {
-    int* f = reinterpret_cast<int*>(smem + L.items + k * L.item_stride + IS.flags);
-    f[0] = 0;
-    f[1] = 0x7fffffff;
-    f[2] = k * p.C;  // turn: first cluster of CTA-local item k
-  }
+  int* fd_count = reinterpret_cast<int*>(smem + L.items);
+  if (fd)
+    for (int k = tid; k < FD_CNT; k += blockDim.x) fd_count[k] = 0;
   // operand tiles start zeroed: pad features (odd U, T < 16) and unused M
   // blocks are never written afterwards
   for (int e = tid; e < 2 * TC_NOP * L.opb / 16; e += blockDim.x)
@@ -766,8 +757,19 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
         else
           linear_unit<UP>(w, a, tm);
-        char* slot = smem + L.items + (il % L.nir) * L.item_stride;
-        fd_fold<UP>(w, slot, IS, p, n, il, c, L.nir, tm);
+        // stash this cluster's estimate, count the arrival; the last of the
+        // item's C clusters folds them in cluster order
+        fd_stash(w, p, n, c, tm);
+        __threadfence_block();
+        tm.sync();
+        int last = 0;
+        if (lane == 0) last = (atomicAdd(&fd_count[il & (FD_CNT - 1)], 1) == p.C - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          if (lane == 0) fd_count[il & (FD_CNT - 1)] = 0;
+          __threadfence_block();
+          fd_finish(reinterpret_cast<float*>(w.X), p, n, tm);
+        }
       }
       tm.sync();
       if (lane == 0) mbar_arrive(&slot_empty[sv]);
