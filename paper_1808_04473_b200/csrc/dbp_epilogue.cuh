@@ -107,103 +107,136 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
 // on the pivot), and the pivot row / column reach the lanes by shuffles, so
 // a step needs neither shared memory nor a barrier.  Padded rows / columns
 // (u < UP) are the identity and stay untouched.
-template <int UP>
-__device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, int lane) {
+// NU independent units are solved together (NU = 2: their pivot chains
+// interleave, hiding the shuffle / reciprocal latency of a lone warp).
+template <int UP, int NU>
+__device__ void linear_solve_warp_n(const Work* w, const EpiArgs* a, const float* rho, int lane) {
   constexpr int RS = 32 / UP;
   constexpr int EPT = UP * UP / 32;
-  const int u = a.u, T = a.T, LD = w.LD;
+  const int u = a[0].u, T = a[0].T, LD = w[0].LD;  // units share the geometry
   const int j = lane % UP, rb = lane / UP;
-  float2 m[EPT];
-  float dgl = 1.f;  // original diagonal of the (at most one) diagonal element this lane owns
+  float2 m[NU][EPT];
+  float dgl[NU];  // original diagonal of the (at most one) diagonal element this lane owns
 #pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int i = rb + r * RS;
-    float2 v;
-    if (i < u && j < u) {
-      v = w.G[i * LD + j];
-      if (i == j) {
-        v.x += rho;
-        v.y = 0.f;
-        dgl = v.x;
+  for (int q = 0; q < NU; ++q) {
+    dgl[q] = 1.f;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = rb + r * RS;
+      float2 v;
+      if (i < u && j < u) {
+        v = w[q].G[i * LD + j];
+        if (i == j) {
+          v.x += rho[q];
+          v.y = 0.f;
+          dgl[q] = v.x;
+        }
+      } else {
+        v = make_float2(i == j ? 1.f : 0.f, 0.f);
       }
-    } else {
-      v = make_float2(i == j ? 1.f : 0.f, 0.f);
+      m[q][r] = v;
     }
-    m[r] = v;
   }
   const float tolf = 8.f * (float)u * FLT_EPSILON;
-  bool bad = false;
+  bool bad[NU];
+#pragma unroll
+  for (int q = 0; q < NU; ++q) bad[q] = false;
   // the pivot loop stays rolled (a small instruction footprint for the
-  // warp-specialized kernel); the pivot row's register is picked by selects,
-  // never by a dynamic register index.  Padded steps k >= u are no-ops.
+  // warp-specialized kernel); the pivot row's register is picked by a select
+  // tree, never by a dynamic register index.  Padded steps k >= u are no-ops.
 #pragma unroll 1
   for (int k = 0; k < u; ++k) {
     const int kr = k / RS, own = (k % RS) * UP + k;  // lane holding (k, k) in register kr
-    float2 mk = m[0];
 #pragma unroll
-    for (int r = 1; r < EPT; ++r)
-      if (r == kr) mk = m[r];
-    float p = __shfl_sync(0xffffffffu, mk.x, own);
-    const float d0 = __shfl_sync(0xffffffffu, dgl, own);
-    if (!(p > tolf * d0)) {
-      bad = true;
-      p = 1.f;
-    }
-    const float rp = 1.f / p;
-    const float2 rkj = shfl2(mk, (k % RS) * UP + j);
-    const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
+    for (int q = 0; q < NU; ++q) {
+      float2 sel[EPT];
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      float2 ci = shfl2(m[r], rb * UP + k);
-      if (rb + r * RS == k) ci = make_float2(p - 1.f, 0.f);
-      c_fms(m[r], ci, rj);
+      for (int r = 0; r < EPT; ++r) sel[r] = m[q][r];
+#pragma unroll
+      for (int bit = 1; bit < EPT; bit <<= 1)
+#pragma unroll
+        for (int r = 0; r + bit < EPT; r += 2 * bit) sel[r] = (kr & bit) ? sel[r + bit] : sel[r];
+      const float2 mk = sel[0];
+      // the pivot owner checks its pivot against the original diagonal and
+      // broadcasts 1 for a failed (singular) pivot
+      float pv = mk.x;
+      if (lane == own && !(pv > tolf * dgl[q])) {
+        bad[q] = true;
+        pv = 1.f;
+      }
+      const float p = __shfl_sync(0xffffffffu, pv, own);
+      const float rp = __frcp_rn(p);
+      const float2 rkj = shfl2(mk, (k % RS) * UP + j);
+      const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        float2 ci = shfl2(m[q][r], rb * UP + k);
+        if (rb + r * RS == k) ci = make_float2(p - 1.f, 0.f);
+        c_fms(m[q][r], ci, rj);
+      }
     }
   }
-  if (bad && lane == 0) set_status(w.flags, ST_SINGULAR);
 #pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int i = rb + r * RS;
-    w.G[i * LD + j] = m[r];
+  for (int q = 0; q < NU; ++q) {
+    if (__any_sync(0xffffffffu, bad[q]) && lane == 0) set_status(w[q].flags, ST_SINGULAR);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) w[q].G[(rb + r * RS) * LD + j] = m[q][r];
   }
   __syncwarp();
   // z = A y_mrc: lane -> UE i = lane % UP, symbols t = rb, rb + RS, ...
-  const bool unb = (a.kind == EQ_LMMSE) && a.unbias;
   const int i = j;
   if (i < u) {
-    float2 arow[UP];
 #pragma unroll
-    for (int c = 0; c < UP; c += 2) {
-      const float4 v = *reinterpret_cast<const float4*>(w.G + i * LD + c);
-      arow[c] = make_float2(v.x, v.y);
-      arow[c + 1] = make_float2(v.z, v.w);
-    }
-    const float aii = w.G[i * LD + i].x;
-    const float cgain = 1.f - rho * aii;
-    const float sc = unb ? 1.f / cgain : 1.f;
-    for (int t = rb; t < T; t += RS) {
-      const float2* zr = w.Z + t * LD;
-      float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;  // two independent chains
+    for (int q = 0; q < NU; ++q) {
+      const bool unb = (a[q].kind == EQ_LMMSE) && a[q].unbias;
+      float2 arow[UP];
 #pragma unroll
       for (int c = 0; c < UP; c += 2) {
-        if (c < u) {
-          const float4 v = *reinterpret_cast<const float4*>(zr + c);
-          c_fma(acc0, arow[c], make_float2(v.x, v.y));
-          if (c + 1 < u) c_fma(acc1, arow[c + 1], make_float2(v.z, v.w));
-        }
+        const float4 v = *reinterpret_cast<const float4*>(w[q].G + i * LD + c);
+        arow[c] = make_float2(v.x, v.y);
+        arow[c + 1] = make_float2(v.z, v.w);
       }
-      w.X[t * LD + i] = c_scale(c_add(acc0, acc1), sc);
-    }
-    if (rb == 0) {
-      if (a.kind == EQ_ZF) {
-        w.s2[i] = a.n0 * aii;
-      } else {
-        w.gn[i] = cgain;
-        if (a.unbias && !(cgain > 0.f)) set_status(w.flags, ST_SINGULAR);
-        w.s2[i] = a.unbias ? a.n0 * aii / cgain : a.n0 * aii;
+      const float aii = w[q].G[i * LD + i].x;
+      const float cgain = 1.f - rho[q] * aii;
+      const float sc = unb ? 1.f / cgain : 1.f;
+      for (int t = rb; t < T; t += 2 * RS) {  // two symbols per pass: independent chains
+        const int t1 = t + RS;
+        const float2* z0 = w[q].Z + t * LD;
+        const float2* z1 = w[q].Z + (t1 < T ? t1 : t) * LD;
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0, acc2 = acc0, acc3 = acc0;
+#pragma unroll
+        for (int c = 0; c < UP; c += 2) {
+          if (c < u) {
+            const float4 v0 = *reinterpret_cast<const float4*>(z0 + c);
+            const float4 v1 = *reinterpret_cast<const float4*>(z1 + c);
+            c_fma(acc0, arow[c], make_float2(v0.x, v0.y));
+            c_fma(acc2, arow[c], make_float2(v1.x, v1.y));
+            if (c + 1 < u) {
+              c_fma(acc1, arow[c + 1], make_float2(v0.z, v0.w));
+              c_fma(acc3, arow[c + 1], make_float2(v1.z, v1.w));
+            }
+          }
+        }
+        w[q].X[t * LD + i] = c_scale(c_add(acc0, acc1), sc);
+        if (t1 < T) w[q].X[t1 * LD + i] = c_scale(c_add(acc2, acc3), sc);
+      }
+      if (rb == 0) {
+        if (a[q].kind == EQ_ZF) {
+          w[q].s2[i] = a[q].n0 * aii;
+        } else {
+          w[q].gn[i] = cgain;
+          if (a[q].unbias && !(cgain > 0.f)) set_status(w[q].flags, ST_SINGULAR);
+          w[q].s2[i] = a[q].unbias ? a[q].n0 * aii / cgain : a[q].n0 * aii;
+        }
       }
     }
   }
   __syncwarp();
+}
+
+template <int UP>
+__device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, int lane) {
+  linear_solve_warp_n<UP, 1>(&w, &a, &rho, lane);
 }
 
 // ---- linear equalizers on (G, Z) -> X (per symbol), s2, gn --------------
