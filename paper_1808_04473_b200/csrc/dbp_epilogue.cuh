@@ -141,39 +141,46 @@ __device__ void linear_solve_warp_n(const Work* w, const EpiArgs* a, const float
   bool bad[NU];
 #pragma unroll
   for (int q = 0; q < NU; ++q) bad[q] = false;
-  // the pivot loop stays rolled (a small instruction footprint for the
-  // warp-specialized kernel); the pivot row's register is picked by a select
-  // tree, never by a dynamic register index.  Padded steps k >= u are no-ops.
+  // Rotating register order: after every RS pivot steps the row registers
+  // rotate by one, so the pivot row is always register 0 (static indices, no
+  // selects); UP steps = EPT full rotations restore the order.  Padded steps
+  // k >= u act on identity rows/columns and are no-ops.  The loop is unrolled
+  // RS-fold only (small instruction footprint).
 #pragma unroll 1
-  for (int k = 0; k < u; ++k) {
-    const int kr = k / RS, own = (k % RS) * UP + k;  // lane holding (k, k) in register kr
+  for (int k0 = 0; k0 < UP; k0 += RS) {
+#pragma unroll
+    for (int kk = 0; kk < RS; ++kk) {
+      const int k = k0 + kk;
+      const int own = kk * UP + k;  // lane holding (k, k), in register 0
+      const bool prow = (rb == kk);  // this lane's register 0 is the pivot row
+#pragma unroll
+      for (int q = 0; q < NU; ++q) {
+        const float2 mk = m[q][0];
+        // the pivot owner checks its pivot against the original diagonal and
+        // broadcasts 1 for a failed (singular) pivot
+        float pv = mk.x;
+        if (lane == own && k < u && !(pv > tolf * dgl[q])) {
+          bad[q] = true;
+          pv = 1.f;
+        }
+        const float p = __shfl_sync(0xffffffffu, pv, own);
+        const float rp = __frcp_rn(p);
+        const float2 rkj = shfl2(mk, kk * UP + j);
+        const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          float2 ci = shfl2(m[q][r], rb * UP + k);
+          if (r == 0 && prow) ci = make_float2(p - 1.f, 0.f);
+          c_fms(m[q][r], ci, rj);
+        }
+      }
+    }
 #pragma unroll
     for (int q = 0; q < NU; ++q) {
-      float2 sel[EPT];
+      const float2 first = m[q][0];
 #pragma unroll
-      for (int r = 0; r < EPT; ++r) sel[r] = m[q][r];
-#pragma unroll
-      for (int bit = 1; bit < EPT; bit <<= 1)
-#pragma unroll
-        for (int r = 0; r + bit < EPT; r += 2 * bit) sel[r] = (kr & bit) ? sel[r + bit] : sel[r];
-      const float2 mk = sel[0];
-      // the pivot owner checks its pivot against the original diagonal and
-      // broadcasts 1 for a failed (singular) pivot
-      float pv = mk.x;
-      if (lane == own && !(pv > tolf * dgl[q])) {
-        bad[q] = true;
-        pv = 1.f;
-      }
-      const float p = __shfl_sync(0xffffffffu, pv, own);
-      const float rp = __frcp_rn(p);
-      const float2 rkj = shfl2(mk, (k % RS) * UP + j);
-      const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rkj, rp);
-#pragma unroll
-      for (int r = 0; r < EPT; ++r) {
-        float2 ci = shfl2(m[q][r], rb * UP + k);
-        if (rb + r * RS == k) ci = make_float2(p - 1.f, 0.f);
-        c_fms(m[q][r], ci, rj);
-      }
+      for (int r = 0; r + 1 < EPT; ++r) m[q][r] = m[q][r + 1];
+      m[q][EPT - 1] = first;
     }
   }
 #pragma unroll
