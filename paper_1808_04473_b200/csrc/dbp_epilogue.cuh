@@ -502,7 +502,8 @@ __device__ __forceinline__ void write_status(const Work& w, const EqParams& p, i
 // decides at run time (SIMT kernels).
 template <int UP, class TM, int CLS = -1>
 __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int cluster, bool item_end,
-                              int& cl_first, const TM& tm, long long* dbg_solve = nullptr) {
+                              int& cl_first, const TM& tm, long long* dbg_solve = nullptr,
+                              float n0_pre = -1.f) {
   constexpr int NT = TM::N;
   const int tid = tm.t;
   const int u = p.u, T = p.T, LD = w.LD;
@@ -515,7 +516,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
     tm.sync();
     return;
   }
-  const float n0 = item_n0(p, n);
+  const float n0 = (n0_pre >= 0.f) ? n0_pre : item_n0(p, n);
   const bool lama = CLS == 2 || (CLS < 0 && p.kind == EQ_LAMA);
   EpiArgs a;
   a.kind = p.kind;

@@ -166,6 +166,7 @@ __device__ void fd_finish(float* scratch, const EqParams& p, int64_t n, const TM
   int st = 0, it = 0x7fffffff;
   for (int e = tm.t; e < wdim; e += TM::N) {
     float dsum = 0.f, hsum = 0.f;
+#pragma unroll 8  // batch the L2 loads of the records
     for (int c = 0; c < C; ++c) {
       const float* rec = recs + (size_t)c * rf;
       const float s2 = __ldcg(rec + 2 * T * u + e);
@@ -196,6 +197,7 @@ __device__ void fd_finish(float* scratch, const EqParams& p, int64_t n, const TM
     const int t = e / u, i = e - t * u;
     const int k = lama ? t : i;
     float2 num = make_float2(0.f, 0.f);
+#pragma unroll 8  // batch the L2 loads of the records
     for (int c = 0; c < C; ++c) {
       const float2 zc = __ldcg(reinterpret_cast<const float2*>(recs + (size_t)c * rf) + e);
       num = c_add(num, c_scale(zc, wts[c * wdim + k]));
@@ -733,20 +735,21 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     for (int u = sv; u < U_tot; u += nsolv, ph ^= 1u) {
       const int64_t n = first + il;
       const bool item_end = (c == upi - 1);
+      const float n0 = item_n0(p, n);  // global load issued before the wait
       wc.wait(&slot_full[sv], ph, 1);
       reset_flags(w, tm);
       tm.sync();
       if (p.ablate & 1) {
       } else if (!fd) {
         const long long t0 = rec ? clock64() : 0;
-        unit_epilogue<UP, Team<32, -1>, CLS>(w, p, n, c, item_end, cl_first, tm, rec ? cnt + 2 : nullptr);
+        unit_epilogue<UP, Team<32, -1>, CLS>(w, p, n, c, item_end, cl_first, tm, rec ? cnt + 2 : nullptr, n0);
         if (rec) cnt[3] += clock64() - t0;
       } else {
         EpiArgs a;
         a.kind = p.kind;
         a.u = p.u;
         a.T = T;
-        a.n0 = item_n0(p, n);
+        a.n0 = n0;
         a.es = p.es;
         a.damping = p.damping;
         a.t_max = p.t_max;
