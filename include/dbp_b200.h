@@ -75,6 +75,11 @@ extern "C" {
 
 int dbp_abi_version(void);
 const char* dbp_last_error(void);
+/* Which fused kernel the calling thread's last dbp_equalize / dbp_gram_mrc
+ * launched: 2 = tensor-core streaming kernel (U <= 32, uniform clusters),
+ * 1 = FP32-SIMT streaming kernel (U = 64 or ragged clusters), 0 = none.
+ * Introspection only (tests and benchmarks); no reference counterpart. */
+int dbp_last_kernel(void);
 int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_bytes);
 
 /* Per-cluster Gram + matched filter.  Replaces local_preprocess

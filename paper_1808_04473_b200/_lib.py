@@ -30,6 +30,7 @@ _i64, _i, _f = C.c_int64, C.c_int, C.c_float
 SIGNATURES = {
     "dbp_abi_version": [],
     "dbp_last_error": [],
+    "dbp_last_kernel": [],
     "dbp_device_query": [_vp, _vp, _vp, _vp],
     "dbp_gram_mrc": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp],
     "dbp_equalize_stats": [_vp, _i64, _i, _i, _i, _f, _vp, _i64, _f, _i, _f, _f, _i, _f,

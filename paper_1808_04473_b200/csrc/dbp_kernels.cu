@@ -147,6 +147,7 @@ __global__ void fuse_estimates_kernel(const float2* __restrict__ z, const float*
 using namespace dbp;
 
 static thread_local std::string g_err;
+static thread_local int g_last_kernel = 0;  // dbp_last_kernel()
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -274,6 +275,8 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   const int item_bytes = p.B * (hrow + yrow);
   int smax = 64 * 1024;
   if (const char* e = getenv("DBP_TC_SMAX")) smax = atoi(e) * 1024;
+  int nsolv = TC_MAX_SOLV;
+  for (int attempt = 0;; ++attempt) {  // shrink the stages until the layout fits
   // (paired items may sit in different stages: the converter waits for both,
   // and the ring keeps at least 2 stages, all filled in order)
   if (item_bytes <= smax) {
@@ -337,15 +340,18 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   };
   // ring depth: ~96 KB of stages when they fit (>= 2), then solver warps
   p.NS = std::max(2, std::min(8, (96 * 1024 + p.stage_bytes - 1) / p.stage_bytes));
-  int nsolv = TC_MAX_SOLV;
+  nsolv = TC_MAX_SOLV;
   // tuning overrides (timing studies only)
   if (const char* e = getenv("DBP_TC_NS")) p.NS = atoi(e);
   if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(2, std::min(TC_MAX_SOLV, atoi(e)));
   while (nsolv > 4 && !fits(p.NS, nsolv)) --nsolv;
   while (p.NS > 2 && !fits(p.NS, nsolv)) --p.NS;
   while (nsolv > 2 && !fits(p.NS, nsolv)) --nsolv;
+  if (fits(p.NS, nsolv)) break;
+  if (attempt == 6 || smax < 8 * 1024) return 1;  // does not fit: caller falls back to the SIMT kernel
+  smax = smax * 3 / 4;
+  }
   const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, p.NS, p.C, lama, fd, nsolv);
-  if (L.total > smem_max) return 1;  // does not fit: caller falls back to the SIMT kernel
   if (fd) {  // per-(item, cluster) fold records: L2-resident scratch, one per stream, grown on demand
     const size_t need = (size_t)p.n_items * p.C * fd_record_floats(p.u, p.T, lama ? p.T : p.u) * sizeof(float);
     p.fd_scratch = static_cast<float*>(stream_scratch(st, need));
@@ -423,9 +429,11 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
       case 16: rc = launch_tc<16>(p, st); break;
       case 32: rc = launch_tc<32>(p, st); break;
     }
+    if (rc == 0) g_last_kernel = 2;
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
     p.NS = up <= 16 ? 4 : 3;
   }
+  g_last_kernel = 1;
   switch (up) {
     case 8: return launch_stream<8, 128>(p, st);
     case 16: return launch_stream<16, 128>(p, st);
@@ -490,6 +498,8 @@ extern "C" {
 int dbp_abi_version(void) { return DBP_ABI_VERSION; }
 
 const char* dbp_last_error(void) { return g_err.c_str(); }
+
+int dbp_last_kernel(void) { return g_last_kernel; }
 
 int dbp_device_query(int* sms, int* major, int* minor, long long* l2) {
   int dev = 0;
