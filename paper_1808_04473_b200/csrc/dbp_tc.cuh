@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       wc.wait(&acc_full[a], (uint32_t)((v >> 1) & 1), 2);
       tc_fence_after();
       const int u_mine = v * pair + hh;
-      if (warp_rows) {
+      if (warp_rows && !(p.ablate & 32)) {  // ablate 32: timing study without the TMEM read-back
         const bool write = has_row && u_mine < U_tot;
         const Work w = work_at(smem, L, hh ? slot[1] : slot[0], UP);
         float* Gf = reinterpret_cast<float*>(w.G);
