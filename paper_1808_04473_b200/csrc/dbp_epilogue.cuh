@@ -51,6 +51,7 @@ struct EqParams {
   // tensor-core kernel staging: a stage is `ips` consecutive whole items
   // (spi == 1) or one row block of one item (spi > 1); H part then Y part
   int ips, spi, stage_bytes, stage_hbytes, stage_ystride;
+  int tc_simple, tc_bc;  // whole-item stages, full 32-row chunks, clusters of tc_bc rows
   int st_row0[MAX_SPI], st_rows[MAX_SPI];
   float* dbg_tile;  // debug: first operand tile of CTA 0 (DBP_TC_DUMP)
   long long* dbg;  // debug: per-role wait-cycle counters [5][4] (DBP_TC_DEBUG)

@@ -335,6 +335,16 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     for (int k = 0; k < p.spi; ++k)
       if (last[k] >= 0) p.chunks[last[k]].flags |= CH_STAGE_REL;
   }
+  // simple geometry: the converter derives every address arithmetically
+  // (chunk j of cluster c starts at row c * B/upi + 32 j) instead of through
+  // the chunk table
+  p.tc_bc = p.B / upi;
+  p.tc_simple = (p.spi == 1) && (p.B % upi == 0);
+  for (int c = 0; p.tc_simple && c < upi; ++c)
+    for (int j = 0; j < cpu; ++j) {
+      const ChunkDesc& cd = p.chunks[c * cpu + j];
+      if (cd.nrows != 32 || cd.row0 != c * p.tc_bc + 32 * j) p.tc_simple = 0;
+    }
   auto fits = [&](int ns, int nsv) {
     return make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, ns, p.C, lama, fd, nsv).total <= smem_max;
   };

@@ -41,12 +41,13 @@
 
 namespace dbp {
 
-constexpr int TC_CONV_W = 4;  // converter warps (2..5)
+constexpr int TC_CONV_SETS = 1;              // converter warp sets, alternating pair-chunks
+constexpr int TC_CONV_W = 4 * TC_CONV_SETS;  // converter warps (2..)
 constexpr int TC_ASM_W = 4;   // assembler warps (6..9)
 constexpr int TC_FIRST_SOLVER = 2 + TC_CONV_W + TC_ASM_W;
 constexpr int TC_MAX_SOLV = 6;
 constexpr int TC_NOP = 2;  // operand tile ring depth (converter -> MMA)
-constexpr int TC_CONV = 32 * TC_CONV_W;
+constexpr int TC_CONV = 128;  // threads of one converter set (barrier arrival count)
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);
 constexpr int FD_CNT = 64;  // FD arrival counters per CTA (items in flight in the solver stage)
@@ -462,7 +463,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // wavefronts, the minimum).  Pad rows/features of the tiles were zeroed at
     // kernel start and are never written.  Full chunks (KC rows) use per-thread
     // task offsets computed once; one iteration converts a whole pair-chunk.
-    const int ct = tid - 64;
+    // two sets of 4 warps convert alternating pair-chunks, so one set's
+    // load / barrier latency overlaps the other's work
+    const int cset = (warp - 2) >> 2;
+    const int ct = ((warp - 2) & 3) * 32 + lane;  // thread index within the set
     const int us2 = 2 * p.us;
     const int hq = p.us / 2;             // float4 per stored H row
     constexpr int HQ = UP / 2;           // float4 slots per H row of the tile
@@ -543,6 +547,64 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         }
       }
       for (int j = 0; j < cpu; ++j) {
+        const int pq = v * cpu + j;
+        if ((pq % TC_CONV_SETS) != cset) continue;
+        b = pq % TC_NOP;
+        bph = (uint32_t)((pq / TC_NOP) & 1);
+        if (p.tc_simple && !(p.ablate & 4)) {
+          // simple geometry: every address is arithmetic (no table lookups:
+          // a lone warp pays ~30 cycles per dependent shared-memory load)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (h < pair && real[h]) wc.wait(&raw_full[gpos[h]], gph[h], 1);
+          if (pq >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
+          const long long t_body = rec ? clock64() : 0;
+          char* hi = smem + L.ops + 2 * b * L.opb;
+          char* lo = hi + L.opb;
+          float4 hv[2][HT], ya[2], yb[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ya[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+            yb[h] = ya[h];
+            if (h >= pair || !real[h]) continue;
+            const int row = cl[h] * p.tc_bc + 32 * j;  // first antenna row of the chunk in its item
+            const char* sb = smem + L.stg + gpos[h] * L.sbytes;
+            const float* Hq = reinterpret_cast<const float*>(sb) + (size_t)(sl[h] * p.B + row) * us2;
+            const float* Yq = reinterpret_cast<const float*>(sb + p.stage_hbytes +
+                                                              (size_t)sl[h] * T * p.stage_ystride) + 2 * row;
+            const int yq = p.stage_ystride / 4;
+#pragma unroll
+            for (int r = 0; r < HT; ++r)
+              if (h_ok[r]) hv[h][r] = *reinterpret_cast<const float4*>(Hq + h_ld[r]);
+            if (y_ok) {
+              ya[h] = *reinterpret_cast<const float4*>(Yq + 2 * ytp * yq + 2 * yk);
+              if (y_ok1) yb[h] = *reinterpret_cast<const float4*>(Yq + (2 * ytp + 1) * yq + 2 * yk);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h >= pair || !real[h]) continue;
+#pragma unroll
+            for (int r = 0; r < HT; ++r)
+              if (h_ok[r]) put(hi, lo, h_st[h][r], hv[h][r]);
+            if (y_ok) {
+              put(hi, lo, y_st[h][0], make_float4(ya[h].x, ya[h].y, yb[h].x, yb[h].y));
+              put(hi, lo, y_st[h][1], make_float4(ya[h].z, ya[h].w, yb[h].z, yb[h].w));
+            }
+          }
+          if (rec) cnt[2] += clock64() - t_body;
+          fence_proxy_async_smem();
+          mbar_arrive(&op_full[b]);
+          // an item's stage is free after its last chunk (multi-item stages:
+          // after the group's last item)
+          if (j == cpu - 1) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (h < pair && real[h] && cl[h] == upi - 1 && (sl[h] == ips - 1 || il[h] == my_items - 1))
+                mbar_arrive(&raw_empty[gpos[h]]);
+          }
+          continue;
+        }
         // wait for the stages of both halves, then for the operand tile
         int sslot[2], sflags[2];
         #pragma unroll
@@ -559,7 +621,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           sslot[h] = pos;
           wc.wait(&raw_full[pos], sp, 1);
         }
-        if (v * cpu + j >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
+        if (pq >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
         const long long t_body = rec ? clock64() : 0;
         char* hi = smem + L.ops + 2 * b * L.opb;
         char* lo = hi + L.opb;
@@ -635,10 +697,6 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           if (!real[h] || !(sflags[h] & CH_STAGE_REL)) continue;
           if (spi == 1 && sl[h] != ips - 1 && il[h] != my_items - 1) continue;
           mbar_arrive(&raw_empty[sslot[h]]);
-        }
-        if (++b == TC_NOP) {
-          b = 0;
-          bph ^= 1u;
         }
       }
     }
