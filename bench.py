@@ -340,6 +340,7 @@ def single_gpu(args, wl, name):
                 det.run(h, y, 0.0, n0_dev, W)
             torch.cuda.synchronize()
     launches = args.steps
+    kernel_id = _lib.lib().dbp_last_kernel()
     up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
     ms = elapsed_ms / args.steps
     bits = bits_per_step(wl)
@@ -415,8 +416,9 @@ def single_gpu(args, wl, name):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": (f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (1 launch/step)" if up <= 32
-                                else "dbp::stream_kernel (1 launch/step)")},
+                     "kernel": (f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (tensor cores, 1 launch/step)"
+                                if kernel_id == 2 else
+                                f"dbp::stream_kernel<{up}> (FP32 SIMT, 1 launch/step)")},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -430,9 +430,15 @@ static int launch_stats(EqParams& p, cudaStream_t st) {
 // U <= 32 -> tensor-core kernel; U = 64 -> SIMT kernel (2(U+T) > 128).
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
-  static const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
+  const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
   const int up = up_for(p.u);
-  if (!force_simt && up <= 32) {
+  const bool force_tc = getenv("DBP_FORCE_TC") && getenv("DBP_FORCE_TC")[0] == '1';
+  // the tensor-core kernel solves one unit per warp: LAMA (10 iterations over
+  // T x U state) and FD-MRC (trivial solves, fold-bound) run faster on the
+  // CTA-cooperative epilogue of the SIMT kernel (measured, tools/gpu_simt_vs_tc.sh)
+  const bool fdk = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
+  const bool tc_ok = force_tc || (p.kind != EQ_LAMA && !(fdk && p.kind == EQ_MRC));
+  if (!force_simt && up <= 32 && tc_ok) {
     int rc = 1;
     switch (up) {
       case 8: rc = launch_tc<8>(p, st); break;

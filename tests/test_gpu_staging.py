@@ -35,6 +35,8 @@ CASES = [
     ("fd", "zf", 4, 256, 8, 16, 14, 6, {"DBP_TC_SMAX": "32", "DBP_TC_NS": "3"}),  # row blocks at cluster pairs
     ("fd", "mrc", 5, 96, 3, 16, 7, 4, {}),                            # odd cluster count: no pairing
     ("fd", "lmmse", 3, 64, 2, 8, 14, 4, {"DBP_TC_NS": "2"}),          # cfg1 shape
+    ("pd", "lama", 3, 128, 4, 16, 14, 4, {}),                          # LAMA epilogue on a solver warp
+    ("fd", "lama", 3, 128, 4, 8, 6, 2, {}),                            # FD LAMA fold
 ]
 CONST = {2: "qpsk", 4: "qam16", 6: "qam64"}
 
@@ -49,10 +51,12 @@ def test_staging_variant_matches_oracle(arch, kind, n, b, c, u, t, bits, env):
     noise = (rng.standard_normal((n, t, b)) + 1j * rng.standard_normal((n, t, b))) * np.sqrt(n0 / 2)
     Y = (np.einsum("nbu,ntu->ntb", H.astype(complex), s) + noise).astype(np.complex64)
     counts = [b // c] * c
+    env = dict(env, DBP_FORCE_TC="1")  # LAMA / FD-MRC default to the SIMT kernel
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
-        det = dbp.detect(arch, kind, H, Y, n0, counts, const)
+        lp = {"t_max": 5} if kind == "lama" else None
+        det = dbp.detect(arch, kind, H, Y, n0, counts, const, lama_params=lp)
         assert _lib.lib().dbp_last_kernel() == 2  # the tensor-core kernel ran
     finally:
         for k, v in old.items():
@@ -61,12 +65,19 @@ def test_staging_variant_matches_oracle(arch, kind, n, b, c, u, t, bits, env):
             else:
                 os.environ[k] = v
     offs = [0] + list(np.cumsum(counts))
-    ref = O.run_batch(arch, kind, H.astype(complex), Y.astype(complex), offs, n0, 1.0, const.symbols)
+    ref = O.run_batch(arch, kind, H.astype(complex), Y.astype(complex), offs, n0, 1.0, const.symbols,
+                      lama_params=lp)
     assert normwise_rel(det.xhat, ref["z"]) < XHAT_TOL, normwise_rel(det.xhat, ref["z"])
-    s2 = np.broadcast_to(det.sigma2[:, None, :], ref["sigma2"].shape)
+    if kind == "lama":
+        s2 = np.broadcast_to(det.sigma2[:, :, None], ref["sigma2"].shape)
+    else:
+        s2 = np.broadcast_to(det.sigma2[:, None, :], ref["sigma2"].shape)
     assert entry_rel(s2, ref["sigma2"]) < SIGMA2_TOL
     nbad, ntot, at_boundary = check_decisions(det.decisions, ref["dec"], ref["z"], det.xhat, const.pam_levels)
     assert at_boundary and nbad <= 1, nbad
     if arch == "fd":
-        nu = np.broadcast_to(det.nu[:, None], ref["nu"].shape)
+        if kind == "lama":
+            nu = np.broadcast_to(np.transpose(det.nu, (0, 2, 1))[:, :, :, None], ref["nu"].shape)
+        else:
+            nu = np.broadcast_to(det.nu[:, None], ref["nu"].shape)
         assert entry_rel(nu, ref["nu"]) < NU_TOL
