@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
         const uint32_t lo = hi + (uint32_t)L.opb;
         const int nk8 = (p.ablate & 2) ? 0 : (cd.nrows + 7) >> 3;
+        const long long t_mma = rec ? clock64() : 0;
         for (int ks = 0; ks < nk8; ++ks) {
           const uint32_t acc = (j == 0 && ks == 0) ? 0u : 1u;
           const uint64_t ah = umma_desc_mn_sw128(hi + ks * 1024, lbo, 512);
@@ -437,6 +438,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           umma_tf32(d, ah, al, idesc, 1u);
           umma_tf32(d, al, ah, idesc, 1u);
         }
+        if (rec) cnt[3] += clock64() - t_mma;
         if (p.ablate & 16) {  // timing study: plain arrives instead of tcgen05.commit
           mbar_arrive(&op_empty[b]);
           if (j == cpu - 1) mbar_arrive(&acc_full[a]);
