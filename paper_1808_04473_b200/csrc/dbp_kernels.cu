@@ -403,7 +403,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     fprintf(stderr, "[dbp tc debug] NS=%d stage=%d B ips=%d spi=%d pair=%d nsolv=%d (cycles summed over CTAs)\n",
             p.NS, p.stage_bytes, p.ips, p.spi, p.pair, nsolv);
     for (int w = 0; w < threads / 32; ++w) {
-      const char* name = w == 0 ? "producer" : w == 1 ? "mma" : w < 2 + TC_CONV_W ? "converter"
+      const char* name = w == 0 ? "producer" : w < TC_FIRST_CONV ? "mma" : w < TC_FIRST_ASM ? "converter"
                          : w < TC_FIRST_SOLVER ? "assembler" : "solver";
       fprintf(stderr, "  w%-2d %-9s total %.3e  c1 %.3e  c2 %.3e  c3 %.3e\n", w, name, (double)h[w * 4],
               (double)h[w * 4 + 1], (double)h[w * 4 + 2], (double)h[w * 4 + 3]);

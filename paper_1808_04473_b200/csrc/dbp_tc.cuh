@@ -43,8 +43,11 @@ namespace dbp {
 
 constexpr int TC_CONV_SETS = 1;              // converter warp sets, alternating pair-chunks
 constexpr int TC_CONV_W = 4 * TC_CONV_SETS;  // converter warps (2..)
-constexpr int TC_ASM_W = 4;   // assembler warps (6..9)
-constexpr int TC_FIRST_SOLVER = 2 + TC_CONV_W + TC_ASM_W;
+constexpr int TC_MMA_W = 1;   // MMA issuer warps (2 = alternate chunks, one partial accumulator each; measured slower overall: fewer solver registers)
+constexpr int TC_ASM_W = 4;   // assembler warps
+constexpr int TC_FIRST_CONV = 1 + TC_MMA_W;
+constexpr int TC_FIRST_ASM = TC_FIRST_CONV + TC_CONV_W;
+constexpr int TC_FIRST_SOLVER = TC_FIRST_ASM + TC_ASM_W;
 constexpr int TC_MAX_SOLV = 6;
 constexpr int TC_NOP = 2;  // operand tile ring depth (converter -> MMA)
 constexpr int TC_CONV = 128;  // threads of one converter set (barrier arrival count)
@@ -285,8 +288,11 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   const int pair = p.pair;
   const int N = pair * 2 * UP;  // MMA N: the H features of both halves
   constexpr int SW = 2 * 2 * UP;  // TMEM columns per accumulator slot (room for pair == 2)
-  constexpr uint32_t TMEM_COLS = (2 * SW <= 32) ? 32 : (2 * SW <= 64) ? 64 : (2 * SW <= 128) ? 128
-                                 : (2 * SW <= 256) ? 256 : 512;
+  // accumulators: 2 buffers (pairs v, v+1) x TC_MMA_W partial sums (one per
+  // MMA issuer warp), column (2 a + m) * SW
+  constexpr int TCOLS = 2 * TC_MMA_W * SW;
+  constexpr uint32_t TMEM_COLS = (TCOLS <= 32) ? 32 : (TCOLS <= 64) ? 64 : (TCOLS <= 128) ? 128
+                                 : (TCOLS <= 256) ? 256 : 512;
   // warp index broadcast from lane 0: the compiler then treats the role
   // branches as warp-uniform, so shuffles inside them compile to plain SHFL
   // instead of divergence-safe COLLECTIVE sequences
@@ -309,6 +315,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   uint64_t* slot_full = acc_empty + 2;
   uint64_t* slot_empty = slot_full + TC_MAX_SOLV;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+  // chunks per unit, and how many MMA warps contribute to each pair's accumulator
+  const int cpu_ = p.nchunks / ((fd || (p.arch == ARCH_STATS && !p.sum_clusters)) ? p.C : 1);
+  const int cpu_mma = cpu_ < TC_MMA_W ? cpu_ : TC_MMA_W;
   ChunkDesc* chunks = reinterpret_cast<ChunkDesc*>(smem + L.chunks);
   int* st_row0 = reinterpret_cast<int*>(chunks + MAX_CHUNKS);
   int* st_rows = st_row0 + MAX_SPI;
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       mbar_init(&op_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_full[b], cpu_mma);
       mbar_init(&acc_empty[b], TC_ASM);
     }
     for (int v = 0; v < nsolv; ++v) {
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
   // blocks are never written afterwards
   for (int e = tid; e < 2 * TC_NOP * L.opb / 16; e += blockDim.x)
     reinterpret_cast<float4*>(smem + L.ops)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);  // allocated / freed by MMA warp 0
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -406,54 +415,52 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 1) {
-    // -------------------------------------------------------- MMA issuer ----
+  } else if (warp < TC_FIRST_CONV) {
+    // ------------------------------------------------------- MMA issuers ----
+    // Warp 1 + mw issues the MMAs of pair-chunks pq = mw (mod 2), i.e. always
+    // tile mw (TC_NOP = 2), into its own partial accumulator of the pair; the
+    // assembler adds the partials.  Two issuing threads overlap one another's
+    // wait / fence / commit latency.
+    const int mw = warp - 1;
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_tf32_mn(128, N);
       const uint32_t lbo = (uint32_t)L.lbo;
       const uint32_t ops = smem_u32(smem + L.ops);
-      int b = 0;
-      uint32_t bph = 0;
-      for (int v = 0, pq = 0; v < n_pairs; ++v)
-        for (int j = 0; j < cpu; ++j, ++pq) {  // one tile per (pair v, chunk j)
-        wc.wait(&op_full[b], bph, 1);
-        if (p.dbg_tile && blockIdx.x == 0 && pq == 0) {
-          const float* t = reinterpret_cast<const float*>(smem + L.ops);
-          for (int e = 0; e < L.opb / 4; ++e) p.dbg_tile[e] = t[e];
-        }
-        const ChunkDesc cd = chunks[j];  // units share the chunk structure
+      for (int v = 0; v < n_pairs; ++v) {
         const int a = v & 1;
-        if (j == 0 && v >= 2) wc.wait(&acc_empty[a], (uint32_t)(((v >> 1) - 1) & 1), 2);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(a * SW);
-        const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
-        const uint32_t lo = hi + (uint32_t)L.opb;
-        const int nk8 = (p.ablate & 2) ? 0 : (cd.nrows + 7) >> 3;
-        const long long t_mma = rec ? clock64() : 0;
-        for (int ks = 0; ks < nk8; ++ks) {
-          const uint32_t acc = (j == 0 && ks == 0) ? 0u : 1u;
-          const uint64_t ah = umma_desc_mn_sw128(hi + ks * 1024, lbo, 512);
-          const uint64_t al = umma_desc_mn_sw128(lo + ks * 1024, lbo, 512);
-          umma_tf32(d, ah, ah, idesc, acc);
-          umma_tf32(d, ah, al, idesc, 1u);
-          umma_tf32(d, al, ah, idesc, 1u);
-        }
-        if (rec) cnt[3] += clock64() - t_mma;
-        if (p.ablate & 16) {  // timing study: plain arrives instead of tcgen05.commit
-          mbar_arrive(&op_empty[b]);
-          if (j == cpu - 1) mbar_arrive(&acc_full[a]);
-        } else {
+        bool first = true;
+        for (int j = 0; j < cpu; ++j) {
+          const int pq = v * cpu + j;
+          if (pq % TC_MMA_W != mw) continue;
+          const int b = pq % TC_NOP;
+          const uint32_t bph = (uint32_t)((pq / TC_NOP) & 1);
+          wc.wait(&op_full[b], bph, 1);
+          const ChunkDesc cd = chunks[j];  // units share the chunk structure
+          if (first && v >= 2) wc.wait(&acc_empty[a], (uint32_t)(((v >> 1) - 1) & 1), 2);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)((TC_MMA_W * a + mw) * SW);
+          const uint32_t hi = ops + (uint32_t)(2 * b * L.opb);
+          const uint32_t lo = hi + (uint32_t)L.opb;
+          const int nk8 = (p.ablate & 2) ? 0 : (cd.nrows + 7) >> 3;
+          const long long t_mma = rec ? clock64() : 0;
+          for (int ks = 0; ks < nk8; ++ks) {
+            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+            const uint64_t ah = umma_desc_mn_sw128(hi + ks * 1024, lbo, 512);
+            const uint64_t al = umma_desc_mn_sw128(lo + ks * 1024, lbo, 512);
+            umma_tf32(d, ah, ah, idesc, acc);
+            umma_tf32(d, ah, al, idesc, 1u);
+            umma_tf32(d, al, ah, idesc, 1u);
+          }
+          if (rec) cnt[3] += clock64() - t_mma;
+          first = false;
+          const bool last_mine = (j + TC_MMA_W >= cpu);  // no later chunk of this pair for this warp
           umma_commit(&op_empty[b]);
-          if (j == cpu - 1) umma_commit(&acc_full[a]);
-        }
-        if (++b == TC_NOP) {
-          b = 0;
-          bph ^= 1u;
+          if (last_mine) umma_commit(&acc_full[a]);
         }
       }
     }
     __syncwarp();
-  } else if (warp < 2 + TC_CONV_W) {
+  } else if (warp < TC_FIRST_ASM) {
     // -------------------------------------------------------- converters ----
     // hi = x with the low 13 mantissa bits cleared (exact TF32), lo = x - hi.
     // H rows: one float4 (2 UEs) per task, written to the same antenna row of
@@ -467,8 +474,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // task offsets computed once; one iteration converts a whole pair-chunk.
     // two sets of 4 warps convert alternating pair-chunks, so one set's
     // load / barrier latency overlaps the other's work
-    const int cset = (warp - 2) >> 2;
-    const int ct = ((warp - 2) & 3) * 32 + lane;  // thread index within the set
+    const int cset = (warp - TC_FIRST_CONV) >> 2;
+    const int ct = ((warp - TC_FIRST_CONV) & 3) * 32 + lane;  // thread index within the set
     const int us2 = 2 * p.us;
     const int hq = p.us / 2;             // float4 per stored H row
     constexpr int HQ = UP / 2;           // float4 slots per H row of the tile
@@ -748,11 +755,20 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         // both halves (e.g. rows 64..95 = Y of half 0 and of half 1): read all
         // pair * 2UP columns and let each thread keep its half's columns
         // [hh * 2UP, (hh + 1) * 2UP)
-        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(a * SW);
+        // partial accumulators of the pair: one per contributing MMA warp
+        // (with one chunk per unit only warp (v mod 2) contributes)
+        const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) +
+                               (uint32_t)((TC_MMA_W * a + (cpu_mma == 1 ? (v * cpu) % TC_MMA_W : 0)) * SW);
         const int rloc = is_h ? (m - hh * 2 * UP) : ((m - YB) & 31);  // row within the half
         for (int c16 = 0; c16 < pair * 2 * UP / 16; ++c16) {
           float vv[16];
           tmem_ld16(taddr + 16 * c16, vv);
+          for (int mm = 1; mm < cpu_mma; ++mm) {
+            float v2[16];
+            tmem_ld16(taddr + mm * SW + 16 * c16, v2);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) vv[c] += v2[c];
+          }
           const int colbase = 8 * c16 - hh * UP;  // UE column of vv[0] within this row's half
           const bool mine = write && colbase >= 0 && colbase < UP;
 #pragma unroll
