@@ -291,19 +291,26 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     linear_solve_warp<UP>(w, a, rho, tid);
     return;
   }
-  // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows
+  // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows.  The
+  // sweep is the branch-free rank-1 update of linear_solve_warp_n
+  //   m_ij -= c_i r_j,  c_i = m_ik (i != k), c_k = p - 1,  r_j = m_kj / p (j != k), r_k = 1 + 1/p,
+  // with rotating register order: after every RS steps the row registers
+  // rotate by one, so the pivot row is always register 0; the pivot column
+  // is published by register slot ([i0][slot], slot = original register).
   constexpr int RS = (NT >= UP) ? NT / UP : 1;
   constexpr int EPT = (UP * UP + NT - 1) / NT;
+  static_assert((EPT & (EPT - 1)) == 0, "rows per thread must be a power of two");
   const int j = tid % UP;
   const int i0 = tid / UP;
+  const bool live = (i0 < UP);  // threads beyond UP*UP elements (NT > UP*UP) idle
   float2 m[EPT];
   float2* rowb = w.W;           // [2][UP] pivot rows (double-buffered)
-  float2* colb = w.W + 2 * UP;  // [2][UP] pivot columns
+  float2* colb = w.W + 2 * UP;  // [2][UP] pivot columns, [i0][slot]
   const float tolf = 8.f * (float)u * FLT_EPSILON;
 #pragma unroll
   for (int r = 0; r < EPT; ++r) {
     const int i = i0 + r * RS;
-    float2 v = make_float2(0.f, 0.f);
+    float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
     if (i < u && j < u) {
       v = w.G[i * LD + j];
       if (i == j) {
@@ -314,38 +321,42 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     }
     m[r] = v;
   }
-  const bool live = (i0 < UP);  // threads beyond UP*UP elements (NT > UP*UP) idle
-  for (int k = 0; k < u; ++k) {
-    float2* rk = rowb + (k & 1) * UP;
-    float2* ck = colb + (k & 1) * UP;
-    if (live) {
+  for (int k0 = 0; k0 < UP; k0 += RS) {
+    const int rot = k0 / RS;  // rotations done so far
+    for (int kk = 0; kk < RS && k0 + kk < UP; ++kk) {
+      const int k = k0 + kk;
+      float2* rk = rowb + (k & 1) * UP;
+      float2* ck = colb + (k & 1) * UP;
+      if (live) {
+        if (i0 == kk) rk[j] = m[0];
+        if (j == k) {
 #pragma unroll
-      for (int r = 0; r < EPT; ++r) {
-        const int i = i0 + r * RS;
-        if (i == k) rk[j] = m[r];
-        if (j == k) ck[i] = m[r];
-      }
-    }
-    tm.sync();
-    float p = rk[k].x;
-    if (!(p > tolf * w.dg[k])) {
-      if (tid == 0) set_status(w.flags, ST_SINGULAR);
-      p = 1.f;
-    }
-    const float rp = 1.f / p;
-    if (live) {
-      const float2 rkj = c_scale(rk[j], rp);
-#pragma unroll
-      for (int r = 0; r < EPT; ++r) {
-        const int i = i0 + r * RS;
-        if (i == k) {
-          m[r] = (j == k) ? make_float2(rp, 0.f) : c_scale(m[r], rp);
-        } else if (j == k) {
-          m[r] = c_scale(m[r], -rp);
-        } else {
-          c_fms(m[r], ck[i], rkj);
+          for (int r = 0; r < EPT; ++r) ck[i0 * EPT + ((r + rot) & (EPT - 1))] = m[r];
         }
       }
+      tm.sync();
+      float p = rk[k].x;
+      if (k < u && !(p > tolf * w.dg[k])) {
+        if (tid == 0) set_status(w.flags, ST_SINGULAR);
+        p = 1.f;
+      }
+      if (k >= u) p = 1.f;  // padded step: identity pivot
+      const float rp = 1.f / p;
+      if (live) {
+        const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rk[j], rp);
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          float2 ci = ck[i0 * EPT + ((r + rot) & (EPT - 1))];
+          if (r == 0 && i0 == kk) ci = make_float2(p - 1.f, 0.f);
+          c_fms(m[r], ci, rj);
+        }
+      }
+    }
+    if (live) {
+      const float2 first = m[0];
+#pragma unroll
+      for (int r = 0; r + 1 < EPT; ++r) m[r] = m[r + 1];
+      m[EPT - 1] = first;
     }
   }
   if (live) {
