@@ -52,6 +52,7 @@ struct EqParams {
   // (spi == 1) or one row block of one item (spi > 1); H part then Y part
   int ips, spi, stage_bytes, stage_hbytes, stage_ystride;
   int tc_simple, tc_bc;  // whole-item stages, full 32-row chunks, clusters of tc_bc rows
+  int g_hermitian;       // G is the kernel's own Gram (exactly Hermitian in shared memory)
   int st_row0[MAX_SPI], st_rows[MAX_SPI];
   float* dbg_tile;  // debug: first operand tile of CTA 0 (DBP_TC_DUMP)
   long long* dbg;  // debug: per-role wait-cycle counters [5][4] (DBP_TC_DEBUG)
@@ -417,7 +418,7 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
 // denoiser (its F, G only feed discarded updates).
 template <class TM>
 __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z, float2* tr_s,
-                          float2* tr_v, float* tr_phi, const TM& tm) {
+                          float2* tr_v, float* tr_phi, const TM& tm, bool herm = false) {
   constexpr int NT = TM::N;
   const int tid = tm.t;
   const int u = a.u, T = a.T, LD = w.LD;
@@ -444,8 +445,16 @@ __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp
       const float2* grow = w.G + i * LD;
       // z = y_mrc + (I - G) s + v
       float2 z = c_add(w.Z[t * LD + i], c_add(srow[i], w.Vv[t * LD + i]));
+      if (herm) {
+        // G Hermitian (the kernel's own Gram): (G s)_i = sum_j conj(G_ji) s_j;
+        // lanes with consecutive i then read consecutive words of row j
+        // (no bank conflicts) and s_j is a broadcast
 #pragma unroll 4
-      for (int j = 0; j < u; ++j) c_fms(z, grow[j], srow[j]);
+        for (int j = 0; j < u; ++j) c_fms_conj(z, w.G[j * LD + i], srow[j]);
+      } else {
+#pragma unroll 4
+        for (int j = 0; j < u; ++j) c_fms(z, grow[j], srow[j]);
+      }
       if (!c_finite(z) || !(c_abs2(z) < DIVERGE_ABS2)) atomicMin(w.flags + 1, it);
       w.X[t * LD + i] = z;
       const float phi = w.phi[t];
@@ -552,7 +561,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
         tv = p.tr_v + o;
         tp = p.tr_phi + (size_t)n * p.t_max * T;
       }
-      lama_unit(w, a, p.cp, tz, ts, tv, tp, tm);
+      lama_unit(w, a, p.cp, tz, ts, tv, tp, tm, p.g_hermitian != 0);
     } else {
       const long long t0 = dbg_solve ? clock64() : 0;
       linear_unit<UP>(w, a, tm);
@@ -593,7 +602,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
   a.lama_scale = p.cl_scale[cluster];
   a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
   if (lama)
-    lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm);
+    lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, p.g_hermitian != 0);
   else
     linear_unit<UP>(w, a, tm);
   // weights: MRC -> Gram diagonal (fusion.py:149-151), otherwise

@@ -430,6 +430,7 @@ static int launch_stats(EqParams& p, cudaStream_t st) {
 // U <= 32 -> tensor-core kernel; U = 64 -> SIMT kernel (2(U+T) > 128).
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
+  p.g_hermitian = 1;  // the streaming kernels build G themselves (full Hermitian matrix)
   const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
   const int up = up_for(p.u);
   const bool force_tc = getenv("DBP_FORCE_TC") && getenv("DBP_FORCE_TC")[0] == '1';
