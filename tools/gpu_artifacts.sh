@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
 timeout 600 python bench.py > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err; tail -1 gpurun_out/bench_cfg2.json | cut -c1-300
-for c in cfg1 cfg3-zf cfg3-mrc cfg4-fd cfg4-pd cfg5-pd512 cfg5-fd512; do
+for c in cfg1 cfg3-zf cfg3-mrc cfg4-fd cfg4-pd cfg5-pd512 cfg5-fd512 cfg5-pd1024 cfg5-fd1024; do
   timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu --e2e-steps 0 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   tail -1 gpurun_out/bench_$c.json | cut -c1-120
 done
