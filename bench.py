@@ -294,20 +294,33 @@ def single_gpu(args, wl, name):
     torch.cuda.set_device(0)
     const = dbp.make_constellation(CONST[wl["bits"]])
     big = wl["U"] == 64
-    H, Y, n0, uf = make_inputs(wl, unique_frames=2 if big else None)
     n_items = wl["frames"] * W
     counts = [wl["B"] // wl["C"]] * wl["C"]
     lp = {"t_max": wl["t_max"]} if wl["kind"] == "lama" else None
     det = dbp.Detector(wl["arch"], wl["kind"], n_items, wl["B"], wl["U"], T, counts, const, lama_params=lp)
-    # device-resident inputs; alternate two copies so no step starts from a warm L2
-    Hd = torch.empty((n_items, wl["B"], wl["U"]), dtype=torch.complex64, device="cuda")
-    Yd = torch.empty((n_items, T, wl["B"]), dtype=torch.complex64, device="cuda")
-    Hu, Yu = torch.from_numpy(H).cuda(), torch.from_numpy(Y).cuda()
-    for f in range(wl["frames"]):
-        src = (f % uf) * W
-        Hd[f * W:(f + 1) * W].copy_(Hu[src:src + W])
-        Yd[f * W:(f + 1) * W].copy_(Yu[src:src + W])
-    del Hu, Yu
+    if big:
+        # cfg5: 25-50 GB of inputs per step are synthesized on the GPU
+        # (dbp_synthesize, counter-based Philox: every frame distinct); a
+        # 2-frame host copy feeds the CPU baseline
+        from paper_1808_04473_b200.synth import snr_to_n0, synth_device
+
+        snr = wl["snr"] if len(wl["snr"]) == wl["frames"] else [wl["snr"][0]] * wl["frames"]
+        n0 = snr_to_n0(snr, const.es)
+        n0_f = torch.tensor(np.asarray(n0, dtype=np.float32), device="cuda")
+        Hd, Yd = synth_device(1234, n_items, wl["B"], wl["U"], T, const, n0_dev=n0_f, n0_group=W)
+        uf = 2
+        H, Y = Hd[:uf * W].cpu().numpy(), Yd[:uf * W].cpu().numpy()
+    else:
+        H, Y, n0, uf = make_inputs(wl)
+        # device-resident inputs; alternate two copies so no step starts from a warm L2
+        Hd = torch.empty((n_items, wl["B"], wl["U"]), dtype=torch.complex64, device="cuda")
+        Yd = torch.empty((n_items, T, wl["B"]), dtype=torch.complex64, device="cuda")
+        Hu, Yu = torch.from_numpy(H).cuda(), torch.from_numpy(Y).cuda()
+        for f in range(wl["frames"]):
+            src = (f % uf) * W
+            Hd[f * W:(f + 1) * W].copy_(Hu[src:src + W])
+            Yd[f * W:(f + 1) * W].copy_(Yu[src:src + W])
+        del Hu, Yu
     step_bytes = (Hd.numel() + Yd.numel()) * 8
     copies = [(Hd, Yd)]
     if step_bytes < 4 * L2_BYTES and torch.cuda.mem_get_info()[0] > 3 * step_bytes:
@@ -363,7 +376,7 @@ def single_gpu(args, wl, name):
 
     # ---------------- end to end: host pinned buffers through the public API
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and step_bytes <= 8 * 2 ** 30:  # pinned host copies of the whole step
         Hh = torch.empty(Hd.shape, dtype=torch.complex64, pin_memory=True)
         Yh = torch.empty(Yd.shape, dtype=torch.complex64, pin_memory=True)
         Hh.copy_(Hd)
@@ -407,7 +420,8 @@ def single_gpu(args, wl, name):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c64 (fp32 arithmetic)",
         "data": "synthetic: i.i.d. Rayleigh CN(0,1/B) channels constant over T, uniform QAM symbols, "
-                "CN(0,N0) noise, seeded (paper's LTE/WINNER-II data not available)",
+                "CN(0,N0) noise, seeded (paper's LTE/WINNER-II data not available)"
+                + ("; generated on the GPU (dbp_synthesize, Philox4x32-10), every frame distinct" if big else ""),
         "config": {"workload": wl_desc(name, wl), "B": wl["B"], "C": wl["C"], "U": wl["U"], "T": T, "W": W,
                    "frames_per_step": wl["frames"], "snr_db": wl["snr"], "items_per_step": n_items,
                    "l2": f"inputs {step_bytes / 2**20:.0f} MiB/step vs 126 MiB L2; {len(copies)} input "

@@ -174,6 +174,17 @@ int dbp_fusion_weights(const float* s2, int64_t n, int C, int u, float* nu, int3
 int dbp_fuse_estimates(const void* z, const float* s2, const float* nu, int C, int64_t count, void* z_out,
                        float* s2_out, void* stream);
 
+/* On-device input synthesis.  Replaces the draws of
+ * run_trial / sample_rayleigh_channel / sample_symbols / transmit
+ * (montecarlo.py:154-160, model.py:207-236) for whole batches on the GPU:
+ * H [n][B][u] ~ CN(0, 1/B), symbol indices [n][T][u] uniform over the M
+ * symbols (complex pairs), Y [n][T][B] = H s + CN(0, N0), N0 = n0 or
+ * n0_dev[(item0 + i) / n0_group].  Counter-based Philox4x32-10 keyed by seed
+ * and the global item index (counter mapping in csrc/dbp_synth.cuh), so any
+ * item range is reproducible independently.  sym may be NULL.  B and u even. */
+int dbp_synthesize(uint64_t seed, int64_t n_items, int64_t item0, int B, int u, int T, const float* symbols, int M,
+                   float n0, const float* n0_dev, int64_t n0_group, void* H, void* Y, uint8_t* sym, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

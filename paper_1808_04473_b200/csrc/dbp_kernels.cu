@@ -22,6 +22,7 @@
 #include "dbp_epilogue.cuh"
 #include "dbp_simt.cuh"
 #include "dbp_tc.cuh"
+#include "dbp_synth.cuh"
 
 namespace dbp {
 
@@ -738,6 +739,26 @@ int dbp_fuse_estimates(const void* z, const float* s2, const float* nu, int C, i
   fuse_estimates_kernel<<<grid_for(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const float2*>(z), s2, nu, C, count, static_cast<float2*>(z_out), s2_out);
   return cuda_check("fuse_estimates_kernel");
+}
+
+// On-device frame synthesis (dbp_synth.cuh): H, Y (and optionally the symbol
+// indices) of items [item0, item0 + n_items).
+int dbp_synthesize(uint64_t seed, int64_t n_items, int64_t item0, int B, int u, int T, const float* symbols, int M,
+                   float n0, const float* n0_dev, int64_t n0_group, void* H, void* Y, uint8_t* sym, void* stream) {
+  if (n_items <= 0) return DBP_OK;
+  if (!H || !Y || !symbols) return fail(DBP_E_ARG, "null pointer");
+  if (B < 2 || (B & 1) || u < 2 || (u & 1) || u > 64) return fail(DBP_E_UNSUPPORTED, "B and u must be even, u <= 64");
+  if (T < 1 || T > MAX_T) return fail(DBP_E_UNSUPPORTED, "T must be in [1, 16]");
+  if (M < 1 || M > MAX_SYMS) return fail(DBP_E_ARG, "constellation size out of range");
+  ConstParams cp;
+  int rc = fill_const(cp, nullptr, 0, symbols, M, 1.f);
+  if (rc) return rc;
+  const int threads = B >= 256 ? 256 : 128;
+  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sm_count() * 8);
+  synth_kernel<<<(unsigned)grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      seed, n_items, item0, B, u, T, cp, n0_dev, n0_group > 0 ? n0_group : 1, n0, static_cast<float2*>(H),
+      static_cast<float2*>(Y), sym);
+  return cuda_check("synth_kernel");
 }
 
 }  // extern "C"

@@ -49,3 +49,25 @@ def synth_frames(seed, frames, w, t, b, u, constellation="qam16", snr_db=10.0):
         Y[sl] = y
         S[sl] = idx
     return H, Y, S, n0
+
+
+def synth_device(seed, n_items, b, u, t, constellation="qam16", n0=0.1, n0_dev=None, n0_group=1, item0=0,
+                 return_symbols=False, stream=None):
+    """Generate H [n][B][U], Y [n][T][B] (complex64 CUDA tensors) -- and the
+    symbol indices [n][T][U] (uint8) when asked -- on the GPU
+    (``dbp_synthesize``, counter-based Philox4x32-10: item i of the batch is
+    global item ``item0 + i`` and depends on nothing else).  Same model as
+    ``synth_frames`` (H ~ CN(0, 1/B), uniform symbols, CN(0, N0) noise), a
+    different random stream."""
+    from . import _dev, _lib
+
+    const = (make_constellation(constellation) if isinstance(constellation, str) else constellation)
+    t_ = _dev.torch()
+    H = t_.empty((n_items, b, u), dtype=t_.complex64, device="cuda")
+    Y = t_.empty((n_items, t, b), dtype=t_.complex64, device="cuda")
+    S = t_.empty((n_items, t, u), dtype=t_.uint8, device="cuda") if return_symbols else None
+    syms = np.ascontiguousarray(np.stack([const.symbols.real, const.symbols.imag], -1).astype(np.float32))
+    _lib.check(_lib.lib().dbp_synthesize(
+        int(seed), int(n_items), int(item0), int(b), int(u), int(t), syms.ctypes.data, int(const.size),
+        float(n0), _lib.ptr(n0_dev), int(n0_group), _lib.ptr(H), _lib.ptr(Y), _lib.ptr(S), _lib.stream_ptr(stream)))
+    return (H, Y, S) if return_symbols else (H, Y)
