@@ -185,6 +185,15 @@ int dbp_fuse_estimates(const void* z, const float* s2, const float* nu, int C, i
 int dbp_synthesize(uint64_t seed, int64_t n_items, int64_t item0, int B, int u, int T, const float* symbols, int M,
                    float n0, const float* n0_dev, int64_t n0_group, void* H, void* Y, uint8_t* sym, void* stream);
 
+/* Soft outputs (no reference counterpart: the
+ * reference stops at hard_detect, equalize.py:262-268).  Gray-labelled bit
+ * LLRs llr [n][T][u][2 log2 L] (log P(b=0)/P(b=1), bits MSB first, label of
+ * symbol k = i L + j is (gray(i) << log2 L) | gray(j), model.gray_labels)
+ * from x-hat [n][T][u] under x = s + CN(0, sigma2); sigma2 is [n][u] or, with
+ * s2_per_symbol, [n][T] (LAMA).  exact = 0: max-log; 1: log-sum-exp. */
+int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int s2_per_symbol, const float* levels,
+            int L, int exact, float* llr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -370,3 +370,39 @@ def message_volume(u, n_sc, n_sym, c, bytes_per_entry=8):
     pd = (u * u * n_sc + u * n_sc * n_sym) * c * bytes_per_entry
     fd = u * n_sc * n_sym * c * bytes_per_entry
     return pd, fd, 2 * fd
+
+
+# --------------------------------------------------------------------------
+# soft outputs (no reference counterpart -- the
+# reference stops at hard decisions, equalize.py:262-268).  Unpinned by
+# construction: checked against closed forms in tests/test_llr_oracle.py.
+# --------------------------------------------------------------------------
+def gray_labels(symbols, levels):
+    """Binary-reflected Gray code of the real-level index (high bits) and the
+    imaginary-level index (low bits) of symbol k = i*L + j."""
+    side = len(levels)
+    half = int(np.log2(side))
+    k = np.arange(len(symbols))
+    i, j = k // side, k % side
+    return ((i ^ (i >> 1)) << half) | (j ^ (j >> 1))
+
+
+def bit_llr(x, s2, symbols, levels, exact=False):
+    """Bit LLRs log P(b=0|x)/P(b=1|x) of the decoupled channel x = s + CN(0,
+    s2), uniform prior, by brute force over all M symbols; bits MSB first.
+    ``x`` and ``s2`` broadcast; output [..., 2 log2 L]."""
+    x = np.asarray(x, dtype=np.complex128)
+    s2 = np.broadcast_to(np.asarray(s2, dtype=float), x.shape)
+    labels = gray_labels(symbols, levels)
+    nb = 2 * int(np.log2(len(levels)))
+    d = np.abs(x[..., None] - np.asarray(symbols)) ** 2 / s2[..., None]
+    out = np.empty(x.shape + (nb,))
+    for b in range(nb):
+        bit = (labels >> (nb - 1 - b)) & 1
+        d0, d1 = d[..., bit == 0], d[..., bit == 1]
+        m0, m1 = d0.min(-1), d1.min(-1)
+        out[..., b] = m1 - m0
+        if exact:
+            out[..., b] += (np.log(np.exp(m0[..., None] - d0).sum(-1))
+                            - np.log(np.exp(m1[..., None] - d1).sum(-1)))
+    return out

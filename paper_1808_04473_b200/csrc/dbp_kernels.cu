@@ -73,6 +73,68 @@ __global__ void hard_detect_kernel(const float2* __restrict__ z, int64_t n, cons
 }
 
 
+
+// Gray-labelled bit LLRs from (x-hat, sigma2) (the
+// reference stops at symbol decisions).  Decoupled model x = s + e,
+// e ~ CN(0, s2); symbol k = i L + j with label (gray(i) << h) | gray(j),
+// h = log2 L, bits MSB first.  Per dimension (the labels factorise):
+// LLR_b = log sum_{a: bit 0} exp(-(v-a)^2/s2) - log sum_{a: bit 1} exp(..)
+// (exact) or its max-log form (min_{bit 1} - min_{bit 0}) / s2.
+__global__ void llr_kernel(const float2* __restrict__ x, const float* __restrict__ s2, int64_t n_el, int T, int u,
+                           int s2_per_symbol, const __grid_constant__ ConstParams cp, int exact,
+                           float* __restrict__ llr) {
+  const int L = cp.L;
+  const int h = 31 - __clz(L);  // log2 L
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = e / ((int64_t)T * u);
+    const int r = (int)(e - item * T * u);
+    const int t = r / u, i = r - t * u;
+    const float var = s2_per_symbol ? s2[item * T + t] : s2[item * u + i];
+    const float inv = 1.f / fmaxf(var, FLT_MIN);
+    const float2 z = x[e];
+    float* out = llr + e * 2 * h;
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const float v = d ? z.y : z.x;
+      float dist[MAX_L];
+#pragma unroll
+      for (int l = 0; l < MAX_L; ++l) {
+        if (l < L) {
+          const float q = v - cp.levels[l];
+          dist[l] = q * q * inv;
+        }
+      }
+      for (int b = 0; b < h; ++b) {  // bit h-1-b of gray(l), MSB first
+        const int sh = h - 1 - b;
+        float m0 = FLT_MAX, m1 = FLT_MAX;
+#pragma unroll
+        for (int l = 0; l < MAX_L; ++l) {
+          if (l < L) {
+            const int bit = ((l ^ (l >> 1)) >> sh) & 1;
+            if (bit) m1 = fminf(m1, dist[l]);
+            else m0 = fminf(m0, dist[l]);
+          }
+        }
+        float v_llr = m1 - m0;  // max-log
+        if (exact) {
+          // log-sum-exp relative to each group's minimum: both sums >= 1, no
+          // underflow however far x is from a group
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+          for (int l = 0; l < MAX_L; ++l) {
+            if (l < L) {
+              if (((l ^ (l >> 1)) >> sh) & 1) s1 += expf(m1 - dist[l]);
+              else s0 += expf(m0 - dist[l]);
+            }
+          }
+          v_llr += logf(s0) - logf(s1);
+        }
+        out[d * h + b] = v_llr;
+      }
+    }
+  }
+}
+
 // ---- small element-wise kernels behind the per-vector drop-in API --------
 // fuse_partials (equalize.py:96-107): out = sum_p parts[p]
 __global__ void stats_sum_kernel(const float2* __restrict__ parts, int P, int64_t count, float2* out) {
@@ -759,6 +821,22 @@ int dbp_synthesize(uint64_t seed, int64_t n_items, int64_t item0, int B, int u, 
       seed, n_items, item0, B, u, T, cp, n0_dev, n0_group > 0 ? n0_group : 1, n0, static_cast<float2*>(H),
       static_cast<float2*>(Y), sym);
   return cuda_check("synth_kernel");
+}
+
+// Bit LLRs [n][T][u][2 log2 L] from x-hat [n][T][u] and sigma2 ([n][u], or
+// [n][T] when s2_per_symbol) for a square QAM set (PAM levels).
+int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int s2_per_symbol, const float* levels,
+            int L, int exact, float* llr, void* stream) {
+  if (n <= 0) return DBP_OK;
+  if (!xhat || !sigma2 || !levels || !llr) return fail(DBP_E_ARG, "null pointer");
+  if (L < 2 || L > MAX_L || (L & (L - 1))) return fail(DBP_E_ARG, "LLRs need a square QAM set (L a power of two)");
+  ConstParams cp;
+  int rc = fill_const(cp, levels, L, nullptr, 0, 1.f);
+  if (rc) return rc;
+  const int64_t n_el = n * T * u;
+  llr_kernel<<<grid_for(n_el), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const float2*>(xhat), sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
+  return cuda_check("llr_kernel");
 }
 
 }  // extern "C"

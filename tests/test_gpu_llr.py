@@ -1,0 +1,43 @@
+"""Gray-labelled bit LLRs (dbp_llr, soft.py) against the oracle's brute force
+over all M symbols (oracle.dbp_oracle.bit_llr): max-log and exact
+(log-sum-exp), per-UE and per-symbol variances, QPSK/16/64-QAM; the hard
+decision implied by the LLR signs equals hard_detect's Gray label."""
+
+import numpy as np
+import pytest
+
+import paper_1808_04473_b200 as dbp
+from oracle import dbp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["qpsk", "qam16", "qam64"])
+@pytest.mark.parametrize("exact", [False, True])
+@pytest.mark.parametrize("per_symbol", [False, True])
+def test_llr_matches_brute_force(name, exact, per_symbol):
+    const = dbp.make_constellation(name)
+    rng = np.random.default_rng(11)
+    n, T, u = 7, 5, 6
+    s = const.symbols[rng.integers(0, const.size, (n, T, u))]
+    s2 = rng.uniform(0.02, 0.5, (n, T) if per_symbol else (n, u))
+    noise = (rng.standard_normal((n, T, u)) + 1j * rng.standard_normal((n, T, u))) * 0.3
+    x = (s + noise).astype(np.complex64)
+    got = dbp.llr(x, s2.astype(np.float32), const, exact=exact)
+    s2b = s2[:, :, None] if per_symbol else s2[:, None, :]
+    ref = O.bit_llr(x, s2b, const.symbols, const.pam_levels, exact)
+    scale = np.maximum(np.abs(ref), 1.0)
+    assert np.max(np.abs(got - ref) / scale) < 1e-4
+
+
+def test_llr_signs_give_the_hard_decision_labels():
+    const = dbp.make_constellation("qam16")
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((50, 4, 8)) + 1j * rng.standard_normal((50, 4, 8))).astype(np.complex64)
+    s2 = np.full((50, 8), 0.1, np.float32)
+    bits = (dbp.llr(x, s2, const) < 0).astype(int)  # LLR < 0 -> bit 1
+    nb = bits.shape[-1]
+    label = (bits * (1 << np.arange(nb - 1, -1, -1))).sum(-1)
+    idx = dbp.hard_detect_index(x.astype(complex), const)
+    # exact ties (x on a midpoint) are measure-zero for continuous x
+    assert np.array_equal(label, dbp.gray_labels(const)[idx])
