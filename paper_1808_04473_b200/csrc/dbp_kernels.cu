@@ -80,58 +80,106 @@ __global__ void hard_detect_kernel(const float2* __restrict__ z, int64_t n, cons
 // h = log2 L, bits MSB first.  Per dimension (the labels factorise):
 // LLR_b = log sum_{a: bit 0} exp(-(v-a)^2/s2) - log sum_{a: bit 1} exp(..)
 // (exact) or its max-log form (min_{bit 1} - min_{bit 0}) / s2.
-__global__ void llr_kernel(const float2* __restrict__ x, const float* __restrict__ s2, int64_t n_el, int T, int u,
-                           int s2_per_symbol, const __grid_constant__ ConstParams cp, int exact,
-                           float* __restrict__ llr) {
-  const int L = cp.L;
-  const int h = 31 - __clz(L);  // log2 L
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = e / ((int64_t)T * u);
-    const int r = (int)(e - item * T * u);
-    const int t = r / u, i = r - t * u;
-    const float var = s2_per_symbol ? s2[item * T + t] : s2[item * u + i];
-    const float inv = 1.f / fmaxf(var, FLT_MIN);
-    const float2 z = x[e];
-    float* out = llr + e * 2 * h;
+//
+// One thread per symbol, H = log2 L a template parameter so the level and bit
+// loops fully unroll; the CTA's 256 x 2H LLRs are staged in shared memory and
+// written back as coalesced float4 rows (a thread's own 2H floats sit at a
+// 8-24 B stride, which scalar stores would scatter over 2H sectors per warp
+// instruction).  Exact mode shares one exp2 per level (relative to the
+// dimension's nearest level) across the H bits and falls back to
+// group-relative sums only where the far group's terms would underflow.
+constexpr int LLR_THREADS = 256;
+
+template <int H>
+__global__ void __launch_bounds__(LLR_THREADS) llr_kernel(const float2* __restrict__ x, const float* __restrict__ s2,
+                                                          int64_t n_el, int T, int u, int s2_per_symbol,
+                                                          const __grid_constant__ ConstParams cp, int exact,
+                                                          float* __restrict__ llr) {
+  constexpr int L = 1 << H, NB = 2 * H;
+  constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
+  __shared__ __align__(16) float tile[LLR_THREADS * NB];
+  float lev[L];
 #pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const float v = d ? z.y : z.x;
-      float dist[MAX_L];
-#pragma unroll
-      for (int l = 0; l < MAX_L; ++l) {
-        if (l < L) {
-          const float q = v - cp.levels[l];
-          dist[l] = q * q * inv;
-        }
+  for (int l = 0; l < L; ++l) lev[l] = cp.levels[l];
+  const uint32_t TU = (uint32_t)(T * u);
+  const bool small = n_el <= 0xffffffffll;
+  for (int64_t e0 = (int64_t)blockIdx.x * LLR_THREADS; e0 < n_el; e0 += (int64_t)gridDim.x * LLR_THREADS) {
+    const int64_t e = e0 + threadIdx.x;
+    if (e < n_el) {
+      int64_t sidx;
+      if (s2_per_symbol) {  // [n][T]: item * T + t = e / u
+        sidx = small ? (int64_t)((uint32_t)e / (uint32_t)u) : e / u;
+      } else {  // [n][u]: item * u + e % u
+        const int64_t item = small ? (int64_t)((uint32_t)e / TU) : e / (int64_t)TU;
+        const uint32_t i = small ? (uint32_t)e % (uint32_t)u : (uint32_t)(e % u);
+        sidx = item * u + i;
       }
-      for (int b = 0; b < h; ++b) {  // bit h-1-b of gray(l), MSB first
-        const int sh = h - 1 - b;
-        float m0 = FLT_MAX, m1 = FLT_MAX;
+      // distances in log2 units: d_l = (v - a_l)^2 / s2 * log2(e)
+      const float inv = LOG2E / fmaxf(__ldg(s2 + sidx), FLT_MIN);
+      const float2 z = x[e];
 #pragma unroll
-        for (int l = 0; l < MAX_L; ++l) {
-          if (l < L) {
-            const int bit = ((l ^ (l >> 1)) >> sh) & 1;
-            if (bit) m1 = fminf(m1, dist[l]);
-            else m0 = fminf(m0, dist[l]);
-          }
+      for (int d = 0; d < 2; ++d) {
+        const float v = d ? z.y : z.x;
+        float dist[L], dmin = FLT_MAX;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const float q = v - lev[l];
+          dist[l] = q * q * inv;
+          dmin = fminf(dmin, dist[l]);
         }
-        float v_llr = m1 - m0;  // max-log
+        float w[L];
         if (exact) {
-          // log-sum-exp relative to each group's minimum: both sums >= 1, no
-          // underflow however far x is from a group
-          float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-          for (int l = 0; l < MAX_L; ++l) {
-            if (l < L) {
-              if (((l ^ (l >> 1)) >> sh) & 1) s1 += expf(m1 - dist[l]);
-              else s0 += expf(m0 - dist[l]);
+          for (int l = 0; l < L; ++l) w[l] = exp2f(dmin - dist[l]);
+        }
+#pragma unroll
+        for (int b = 0; b < H; ++b) {  // bit H-1-b of gray(l), MSB first
+          const int sh = H - 1 - b;
+          float m0 = FLT_MAX, m1 = FLT_MAX, s0 = 0.f, s1 = 0.f;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            if (((l ^ (l >> 1)) >> sh) & 1) {
+              m1 = fminf(m1, dist[l]);
+              if (exact) s1 += w[l];
+            } else {
+              m0 = fminf(m0, dist[l]);
+              if (exact) s0 += w[l];
             }
           }
-          v_llr += logf(s0) - logf(s1);
+          float r = m1 - m0;  // max-log, log2 units
+          if (exact) {
+            // log2 sum_{g} 2^(dmin - d) = (dmin - m_g) + log2 sum_g 2^(m_g - d);
+            // the far group's shared sum underflows once m_g - dmin > ~100:
+            // recompute it relative to its own minimum there
+            if (fmaxf(m0, m1) - dmin > 100.f) {
+              const int far = m1 > m0;
+              const float mf = far ? m1 : m0;
+              float sf = 0.f;
+#pragma unroll
+              for (int l = 0; l < L; ++l)
+                if (((((l ^ (l >> 1)) >> sh) & 1) == far)) sf += exp2f(mf - dist[l]);
+              // LLR = log2 s0' - log2 s1' + (m1 - m0) with s_g' group-relative
+              const float sn = far ? s0 : s1;  // near group, relative to dmin = its min
+              r += far ? (__log2f(sn) - __log2f(sf)) : (__log2f(sf) - __log2f(sn));
+            } else {
+              r = __log2f(s0) - __log2f(s1);
+            }
+          }
+          tile[threadIdx.x * NB + d * H + b] = r * LN2;
         }
-        out[d * h + b] = v_llr;
       }
     }
+    __syncthreads();
+    const int64_t cnt = min((int64_t)LLR_THREADS, n_el - e0) * NB;  // floats in this tile
+    float* dst = llr + e0 * NB;
+    if (cnt == LLR_THREADS * NB) {
+      const float4* src4 = reinterpret_cast<const float4*>(tile);
+      float4* dst4 = reinterpret_cast<float4*>(dst);
+      for (int q = threadIdx.x; q < LLR_THREADS * NB / 4; q += LLR_THREADS) dst4[q] = src4[q];
+    } else {
+      for (int q = threadIdx.x; q < cnt; q += LLR_THREADS) dst[q] = tile[q];
+    }
+    __syncthreads();
   }
 }
 
@@ -834,8 +882,12 @@ int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int 
   int rc = fill_const(cp, levels, L, nullptr, 0, 1.f);
   if (rc) return rc;
   const int64_t n_el = n * T * u;
-  llr_kernel<<<grid_for(n_el), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const float2*>(xhat), sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
+  const int64_t grid = std::min<int64_t>((n_el + LLR_THREADS - 1) / LLR_THREADS, (int64_t)sm_count() * 8);
+  auto cs = static_cast<cudaStream_t>(stream);
+  auto xp = static_cast<const float2*>(xhat);
+  if (L == 2) llr_kernel<1><<<(unsigned)grid, LLR_THREADS, 0, cs>>>(xp, sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
+  else if (L == 4) llr_kernel<2><<<(unsigned)grid, LLR_THREADS, 0, cs>>>(xp, sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
+  else llr_kernel<3><<<(unsigned)grid, LLR_THREADS, 0, cs>>>(xp, sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
   return cuda_check("llr_kernel");
 }
 
