@@ -92,6 +92,7 @@ struct EpiArgs {
   float beta, lama_scale, damping;
   int t_max;
   bool unbias;
+  int ablate;  // timing studies only (EqParams::ablate)
 };
 
 __device__ __forceinline__ void set_status(int* flags, int st) { atomicCAS(flags, 0, st); }
@@ -412,14 +413,154 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
   tm.sync();
 }
 
+// ---- LAMA, group-owned symbols (u <= 32) -----------------------------------
+// The T recursions of lama_equalize are independent per OFDM symbol and only
+// share G (read-only), so each group of GS lanes (GS = u rounded up to a power
+// of two, within one warp) owns whole symbols: lane i keeps z, s, v of UE i in
+// registers, the s rows are published through shared memory for the matvec
+// (broadcast reads), and the per-symbol mean of g is a shuffle reduction --
+// no team barrier inside the t_max iterations.  A group can run K symbols'
+// recursions interleaved (independent dependency chains, one G load feeding
+// all); K = 1 measured best (K = 2 costs the second CTA per SM).  lama_scale
+// is applied to the matvec result and to y_mrc
+// instead of rescaling G in place.
+template <int GS, class TM>
+__device__ void lama_unit_groups(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z, float2* tr_s,
+                                 float2* tr_v, float* tr_phi, const TM& tm, bool herm) {
+  constexpr int NT = TM::N;
+  constexpr int NG = NT / GS;  // groups in the team
+  constexpr int K = 1;         // symbols per group and round (2: 169 regs, one CTA per SM, slower)
+  const int tid = tm.t;
+  const int i = tid & (GS - 1), g = tid / GS;
+  const int u = a.u, T = a.T, LD = w.LD;
+  const int ic = i < u ? i : 0;
+  const float sc = a.lama_scale;
+  const float n0 = a.n0 * sc;
+  const float beta = a.beta, damp = a.damping;
+  const float inv_u = 1.f / (float)u;
+  // warp-uniform trip count: slots without a symbol in the last round run a
+  // clamped symbol and write nothing (the shuffles need every lane)
+  const int rounds = (T + K * NG - 1) / (K * NG);
+  for (int r = 0; r < rounds; ++r) {
+    int t[K];
+    bool act[K], live[K];
+    const float2* srow[K];
+    float2 zy[K], s[K], v[K], z[K];
+    float phi[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int tq = g + (r * K + k) * NG;
+      live[k] = tq < T;
+      t[k] = live[k] ? tq : T - 1;
+      act[k] = live[k] && i < u;
+      srow[k] = w.Sv + t[k] * LD;
+      zy[k] = c_scale(w.Z[t[k] * LD + ic], sc);
+      s[k] = cp.mean;
+      v[k] = make_float2(0.f, 0.f);
+      phi[k] = cp.es;
+      if (act[k]) w.Sv[t[k] * LD + i] = s[k];
+    }
+    __syncwarp();
+    for (int it = 1;; ++it) {
+      // z = y_mrc + (I - G) s + v
+      float2 m[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) m[k] = make_float2(0.f, 0.f);
+      int j = 0;
+      if (herm) {
+#pragma unroll 2
+        for (; j + 1 < u; j += 2) {
+          const float2 g0 = w.G[j * LD + ic], g1 = w.G[(j + 1) * LD + ic];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float4 sj = *reinterpret_cast<const float4*>(srow[k] + j);
+            c_fma_conj(m[k], g0, make_float2(sj.x, sj.y));
+            c_fma_conj(m[k], g1, make_float2(sj.z, sj.w));
+          }
+        }
+        if (j < u) {
+          const float2 g0 = w.G[j * LD + ic];
+#pragma unroll
+          for (int k = 0; k < K; ++k) c_fma_conj(m[k], g0, srow[k][j]);
+        }
+      } else {
+        const float2* grow = w.G + ic * LD;
+#pragma unroll 2
+        for (; j + 1 < u; j += 2) {
+          const float4 gj = *reinterpret_cast<const float4*>(grow + j);
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const float4 sj = *reinterpret_cast<const float4*>(srow[k] + j);
+            c_fma(m[k], make_float2(gj.x, gj.y), make_float2(sj.x, sj.y));
+            c_fma(m[k], make_float2(gj.z, gj.w), make_float2(sj.z, sj.w));
+          }
+        }
+        if (j < u) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) c_fma(m[k], grow[j], srow[k][j]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        z[k] = c_sub(c_add(zy[k], c_add(s[k], v[k])), c_scale(m[k], sc));
+        if (act[k] && (!c_finite(z[k]) || !(c_abs2(z[k]) < DIVERGE_ABS2))) atomicMin(w.flags + 1, it);
+        if (tr_z && act[k]) {
+          const size_t o = ((size_t)(it - 1) * T + t[k]) * u + i;
+          tr_z[o] = z[k];
+          tr_s[o] = s[k];
+          tr_v[o] = v[k];
+          if (i == 0) tr_phi[(size_t)(it - 1) * T + t[k]] = phi[k];
+        }
+      }
+      if (it == a.t_max) break;
+      float2 F[K];
+      float gv[K], tau[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        tau[k] = n0 + beta * phi[k];
+        posterior(z[k], tau[k], cp, F[k], gv[k]);
+        gv[k] = act[k] ? gv[k] : 0.f;
+      }
+#pragma unroll
+      for (int o = GS / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) gv[k] += __shfl_xor_sync(0xffffffffu, gv[k], o);
+      }
+      __syncwarp();  // every lane has read the old rows
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float phin = gv[k] * inv_u;
+        const float coef = beta * phin / tau[k];
+        phi[k] = phin;
+        v[k] = c_scale(c_sub(z[k], s[k]), coef);
+        s[k] = c_add(c_scale(F[k], damp), c_scale(s[k], 1.f - damp));
+        if (act[k]) w.Sv[t[k] * LD + i] = s[k];
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (act[k]) w.X[t[k] * LD + i] = z[k];
+      if (live[k] && i == 0) w.s2[t[k]] = n0 + beta * phi[k];
+    }
+  }
+  tm.sync();
+}
+
 // ---- LAMA (equalize.py:208-259) on (G, Z) scaled by lama_scale ----------
 // Per OFDM symbol t an independent recursion; state in shared memory.
 // Output: X = z^{t_max}, s2[t] = tau^{t_max}.  The last iteration skips the
 // denoiser (its F, G only feed discarded updates).
-template <class TM>
+template <int UP = 0, class TM>
 __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z, float2* tr_s,
                           float2* tr_v, float* tr_phi, const TM& tm, bool herm = false) {
   constexpr int NT = TM::N;
+  // group-owned schedule with GS = UP lanes per symbol (one instantiation per
+  // kernel keeps the register budget of the kernel's other phases);
+  // ablate bit 64 selects the team-wide schedule below (timing studies)
+  if constexpr (UP > 0 && UP <= 32 && NT % 32 == 0) {
+    if (!(a.ablate & 64) && a.u <= UP) return lama_unit_groups<UP>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+  }
   const int tid = tm.t;
   const int u = a.u, T = a.T, LD = w.LD;
   const float sc = a.lama_scale;
@@ -547,6 +688,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
   a.es = p.es;
   a.damping = p.damping;
   a.t_max = p.t_max;
+  a.ablate = p.ablate;
   if (p.arch == ARCH_PD) {
     a.beta = p.beta;
     a.lama_scale = p.lama_scale;
@@ -561,7 +703,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
         tv = p.tr_v + o;
         tp = p.tr_phi + (size_t)n * p.t_max * T;
       }
-      lama_unit(w, a, p.cp, tz, ts, tv, tp, tm, p.g_hermitian != 0);
+      lama_unit<UP>(w, a, p.cp, tz, ts, tv, tp, tm, p.g_hermitian != 0);
     } else {
       const long long t0 = dbg_solve ? clock64() : 0;
       linear_unit<UP>(w, a, tm);
@@ -602,7 +744,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
   a.lama_scale = p.cl_scale[cluster];
   a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
   if (lama)
-    lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, p.g_hermitian != 0);
+    lama_unit<UP>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, p.g_hermitian != 0);
   else
     linear_unit<UP>(w, a, tm);
   // weights: MRC -> Gram diagonal (fusion.py:149-151), otherwise

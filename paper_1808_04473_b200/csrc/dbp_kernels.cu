@@ -315,7 +315,9 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
   if (S < 1) return fail(DBP_E_UNSUPPORTED, "too many output tiles for the CTA (u, T too large)");
   const int red_f2 = S > 1 ? (S - 1) * ntiles * 16 : 0;
   const SimtLayout L = make_simt_layout(UP, p.TP, p.stage_f2 * 8, p.NS, p.C, red_f2, lama, fd);
-  auto kern = stream_kernel<UP, NT>;
+  auto kern = p.arch == ARCH_STATS ? stream_kernel<UP, NT, 0>
+              : p.kind == EQ_LAMA   ? stream_kernel<UP, NT, 2>
+                                    : stream_kernel<UP, NT, -1>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   int per_sm = 0;

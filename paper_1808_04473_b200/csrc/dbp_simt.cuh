@@ -223,7 +223,9 @@ __device__ __forceinline__ void reduce_tiles(float2 (&acc)[4][4], const TileInfo
 }
 
 // Persistent streaming kernel: (H, Y) -> stats | PD outputs | FD outputs.
-template <int UP, int NT>
+// CLS: epilogue class (0 stats, 1 linear, 2 LAMA), one instantiation each so
+// a kernel carries (and allocates registers for) only its own epilogue.
+template <int UP, int NT, int CLS>
 __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
     }
     const float2* Hs = reinterpret_cast<const float2*>(smem + L.stages + s * stage_bytes);
     const float2* Ys = Hs + p.KC * p.us;
-    if (ti.active) accumulate_chunk(acc, Hs, Ys, cd.nrows, p.us, p.KCP, ti);
+    if (ti.active && !(p.ablate & 2)) accumulate_chunk(acc, Hs, Ys, cd.nrows, p.us, p.KCP, ti);
     __syncthreads();  // stage s consumed
     if (tid == 0) issue(q + p.NS);
 
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
     const bool unit_end = item_end || (per_cluster && (cd.flags & CH_CLUSTER_END));
     if (!unit_end) continue;
     reduce_tiles<UP, NT>(acc, ti, red, w, p.T, ntiles);
-    unit_epilogue<UP>(w, p, n, cd.cluster, item_end, cl_first, tm);
+    if (!(p.ablate & 1)) unit_epilogue<UP, Team<NT, 0>, CLS>(w, p, n, cd.cluster, item_end, cl_first, tm);
     __syncthreads();
   }
 }

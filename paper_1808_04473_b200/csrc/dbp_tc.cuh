@@ -832,8 +832,9 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         a.beta = p.cl_beta[c];
         a.lama_scale = p.cl_scale[c];
         a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
+        a.ablate = p.ablate;
         if constexpr (lama)
-          lama_unit(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, true);
+          lama_unit<UP>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, true);
         else
           linear_unit<UP>(w, a, tm);
         // stash this cluster's estimate, count the arrival; the last of the
