@@ -424,7 +424,7 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
 // all); K = 1 measured best (K = 2 costs the second CTA per SM).  lama_scale
 // is applied to the matvec result and to y_mrc
 // instead of rescaling G in place.
-template <int GS, class TM>
+template <int GS, int PL, class TM>
 __device__ void lama_unit_groups(const Work& w, const EpiArgs& a, const ConstParams& cp, float2* tr_z, float2* tr_s,
                                  float2* tr_v, float* tr_phi, const TM& tm, bool herm) {
   constexpr int NT = TM::N;
@@ -518,7 +518,7 @@ __device__ void lama_unit_groups(const Work& w, const EpiArgs& a, const ConstPar
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         tau[k] = n0 + beta * phi[k];
-        posterior(z[k], tau[k], cp, F[k], gv[k]);
+        posterior_t<PL>(z[k], tau[k], cp, F[k], gv[k]);
         gv[k] = act[k] ? gv[k] : 0.f;
       }
 #pragma unroll
@@ -559,7 +559,12 @@ __device__ void lama_unit(const Work& w, const EpiArgs& a, const ConstParams& cp
   // kernel keeps the register budget of the kernel's other phases);
   // ablate bit 64 selects the team-wide schedule below (timing studies)
   if constexpr (UP > 0 && UP <= 32 && NT % 32 == 0) {
-    if (!(a.ablate & 64) && a.u <= UP) return lama_unit_groups<UP>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+    if (!(a.ablate & 64) && a.u <= UP) {  // PL: PAM levels per dimension (0: generic set)
+      if (cp.L == 4) return lama_unit_groups<UP, 4>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+      if (cp.L == 8) return lama_unit_groups<UP, 8>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+      if (cp.L == 2) return lama_unit_groups<UP, 2>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+      return lama_unit_groups<UP, 0>(w, a, cp, tr_z, tr_s, tr_v, tr_phi, tm, herm);
+    }
   }
   const int tid = tm.t;
   const int u = a.u, T = a.T, LD = w.LD;
