@@ -314,14 +314,29 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
   const int S = NT / ntiles;
   if (S < 1) return fail(DBP_E_UNSUPPORTED, "too many output tiles for the CTA (u, T too large)");
   const int red_f2 = S > 1 ? (S - 1) * ntiles * 16 : 0;
-  const SimtLayout L = make_simt_layout(UP, p.TP, p.stage_f2 * 8, p.NS, p.C, red_f2, lama, fd);
   auto kern = p.arch == ARCH_STATS ? stream_kernel<UP, NT, 0>
               : p.kind == EQ_LAMA   ? stream_kernel<UP, NT, 2>
                                     : stream_kernel<UP, NT, -1>;
+  // ring depth: the deepest ring (<= p.NS, >= 2) that still lets a second CTA
+  // share the SM, so one CTA's Gram overlaps the other's epilogue (U = 64:
+  // 3 stages = one CTA per SM; 2 stages = two, cfg5 57 -> 46 ms)
+  int per_sm = 0, ns = p.NS;
+  if (const char* e = getenv("DBP_SIMT_NS")) ns = std::max(2, atoi(e));  // tuning studies
+  SimtLayout L = make_simt_layout(UP, p.TP, p.stage_f2 * 8, ns, p.C, red_f2, lama, fd);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
-  int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, L.total);
+  for (int k = ns - 1; k >= 2 && per_sm < 2 && !getenv("DBP_SIMT_NS"); --k) {
+    const SimtLayout L2 = make_simt_layout(UP, p.TP, p.stage_f2 * 8, k, p.C, red_f2, lama, fd);
+    int per2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, kern, NT, L2.total);
+    if (per2 > per_sm) {
+      ns = k;
+      L = L2;
+      per_sm = per2;
+    }
+  }
+  p.NS = ns;
   if (per_sm < 1) return fail(DBP_E_UNSUPPORTED, "kernel does not fit on an SM");
   const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count() * per_sm);
   kern<<<(unsigned)grid, NT, L.total, st>>>(p);
