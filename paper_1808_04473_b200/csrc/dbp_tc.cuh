@@ -833,6 +833,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         a.lama_scale = p.cl_scale[c];
         a.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
         a.ablate = p.ablate;
+        const long long t0 = rec ? clock64() : 0;
         if constexpr (lama)
           lama_unit<UP>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, true);
         else
@@ -842,13 +843,16 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         fd_stash(w, p, n, c, tm);
         __threadfence_block();
         tm.sync();
+        if (rec) cnt[2] += clock64() - t0;  // FD: solve + stash (c2), fold (c3)
         int last = 0;
         if (lane == 0) last = (atomicAdd(&fd_count[il & (FD_CNT - 1)], 1) == p.C - 1);
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           if (lane == 0) fd_count[il & (FD_CNT - 1)] = 0;
           __threadfence_block();
+          const long long t1 = rec ? clock64() : 0;
           fd_finish(reinterpret_cast<float*>(w.X), p, n, tm);
+          if (rec) cnt[3] += clock64() - t1;
         }
       }
       tm.sync();
