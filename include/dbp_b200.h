@@ -194,6 +194,12 @@ int dbp_synthesize(uint64_t seed, int64_t n_items, int64_t item0, int B, int u, 
 int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int s2_per_symbol, const float* levels,
             int L, int exact, float* llr, void* stream);
 
+/* Hard Gray bits (the north star's "hard decisions as indices plus Gray
+ * bits"; SURVEY.md 8(b) dbp_demap bits_out): bits [n][2 log2 L], one byte per
+ * bit, MSB first, of symbol indices idx [n] (uint8 decisions when
+ * idx_bytes = 1, int32 hard_detect indices when 4); label as in dbp_llr. */
+int dbp_gray_bits(const void* idx, int idx_bytes, int64_t n, int L, uint8_t* bits, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -183,6 +183,23 @@ __global__ void __launch_bounds__(LLR_THREADS) llr_kernel(const float2* __restri
   }
 }
 
+// Gray bits of hard decisions (the north star's "hard decisions as indices
+// plus Gray bits"): symbol index k = i L + j -> label (gray(i) << h) | gray(j),
+// h = log2 L, written MSB first as one byte per bit, bits [n][2h].  Indices
+// outside [0, L^2) (never produced by the slicers) give all-ones rows.
+template <typename IDX>
+__global__ void gray_bits_kernel(const IDX* __restrict__ idx, int64_t n, int h, uint8_t* __restrict__ bits) {
+  const int L = 1 << h, nb = 2 * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)idx[e];
+    const bool ok = k >= 0 && k < L * L;
+    const int i = k >> h, j = k & (L - 1);
+    const int label = ok ? (((i ^ (i >> 1)) << h) | (j ^ (j >> 1))) : (1 << nb) - 1;
+    uint8_t* o = bits + e * nb;
+    for (int b = 0; b < nb; ++b) o[b] = (uint8_t)((label >> (nb - 1 - b)) & 1);
+  }
+}
+
 // ---- small element-wise kernels behind the per-vector drop-in API --------
 // fuse_partials (equalize.py:96-107): out = sum_p parts[p]
 __global__ void stats_sum_kernel(const float2* __restrict__ parts, int P, int64_t count, float2* out) {
@@ -906,6 +923,22 @@ int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int 
   else if (L == 4) llr_kernel<2><<<(unsigned)grid, LLR_THREADS, 0, cs>>>(xp, sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
   else llr_kernel<3><<<(unsigned)grid, LLR_THREADS, 0, cs>>>(xp, sigma2, n_el, T, u, s2_per_symbol, cp, exact, llr);
   return cuda_check("llr_kernel");
+}
+
+// Gray bits [n][2 log2 L] (one byte per bit, MSB first) of symbol indices
+// (idx_bytes = 1: uint8 decisions; 4: int32 hard_detect indices).
+int dbp_gray_bits(const void* idx, int idx_bytes, int64_t n, int L, uint8_t* bits, void* stream) {
+  if (n <= 0) return DBP_OK;
+  if (!idx || !bits) return fail(DBP_E_ARG, "null pointer");
+  if (L < 2 || L > MAX_L || (L & (L - 1))) return fail(DBP_E_ARG, "Gray bits need a square QAM set (L a power of two)");
+  if (idx_bytes != 1 && idx_bytes != 4) return fail(DBP_E_ARG, "index type must be uint8 or int32");
+  const int h = 31 - __builtin_clz(L);
+  auto cs = static_cast<cudaStream_t>(stream);
+  if (idx_bytes == 1)
+    gray_bits_kernel<<<grid_for(n), 256, 0, cs>>>(static_cast<const uint8_t*>(idx), n, h, bits);
+  else
+    gray_bits_kernel<<<grid_for(n), 256, 0, cs>>>(static_cast<const int32_t*>(idx), n, h, bits);
+  return cuda_check("gray_bits_kernel");
 }
 
 }  // extern "C"

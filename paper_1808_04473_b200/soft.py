@@ -8,6 +8,9 @@ reports (unbiased linear outputs, or LAMA's z with tau).  Labels are
 gray(j), bits MSB first.  LLR = log P(b=0 | x) / P(b=1 | x); ``exact``
 selects log-sum-exp over the symbols instead of max-log.  Computed by the
 ``dbp_llr`` kernel (one thread per symbol, per-dimension factorisation).
+
+``gray_bits`` gives the hard counterpart: the Gray bits of symbol decisions
+(``Detection.decisions`` or ``hard_detect_index``), ``dbp_gray_bits``.
 """
 
 from __future__ import annotations
@@ -44,3 +47,26 @@ def llr(xhat, sigma2, constellation, exact=False):
     _lib.check(_lib.lib().dbp_llr(_lib.ptr(x), _lib.ptr(s2), n, T, u, per_symbol, lp, L, int(bool(exact)),
                                   _lib.ptr(out), _lib.stream_ptr()))
     return _dev.out(out, host, real=True)
+
+
+def gray_bits(decisions, constellation):
+    """Hard Gray bits [..., 2 log2 L] (uint8 0/1, MSB first) of symbol indices
+    (k = i*L + j; uint8 detector decisions or int32/int64 hard_detect_index
+    output).  Host arrays in -> NumPy out; CUDA tensors in -> CUDA tensor out."""
+    if not getattr(constellation, "is_square_qam", False):
+        raise ConfigError("Gray bits need a square QAM constellation")
+    t = _dev.torch()
+    L = len(constellation.pam_levels)
+    nbits = 2 * int(round(np.log2(L)))
+    _lib.lib()
+    host = not _dev.is_device(decisions)
+    d = decisions if isinstance(decisions, t.Tensor) else t.from_numpy(np.ascontiguousarray(decisions))
+    if d.dtype == t.uint8:
+        idx, width = d.to("cuda").contiguous(), 1
+    elif d.dtype in (t.int32, t.int64, t.int16):
+        idx, width = d.to(device="cuda", dtype=t.int32).contiguous(), 4
+    else:
+        raise ConfigError("decisions must be integer symbol indices")
+    out = t.empty(tuple(idx.shape) + (nbits,), dtype=t.uint8, device="cuda")
+    _lib.check(_lib.lib().dbp_gray_bits(_lib.ptr(idx), width, idx.numel(), L, _lib.ptr(out), _lib.stream_ptr()))
+    return out.cpu().numpy() if host else out

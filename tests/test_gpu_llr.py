@@ -41,3 +41,37 @@ def test_llr_signs_give_the_hard_decision_labels():
     idx = dbp.hard_detect_index(x.astype(complex), const)
     # exact ties (x on a midpoint) are measure-zero for continuous x
     assert np.array_equal(label, dbp.gray_labels(const)[idx])
+
+
+@pytest.mark.parametrize("name", ["qpsk", "qam16", "qam64"])
+def test_gray_bits_match_labels(name):
+    """dbp_gray_bits of the detector's uint8 decisions and of int64 indices
+    equal model.gray_labels unpacked MSB first."""
+    const = dbp.make_constellation(name)
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, const.size, (9, 14, 5))
+    nb = 2 * int(np.log2(len(const.pam_levels)))
+    ref = (dbp.gray_labels(const)[idx][..., None] >> np.arange(nb - 1, -1, -1)) & 1
+    assert np.array_equal(dbp.gray_bits(idx, const), ref)
+    assert np.array_equal(dbp.gray_bits(idx.astype(np.uint8), const), ref)
+    import torch
+    dev = dbp.gray_bits(torch.as_tensor(idx.astype(np.uint8), device="cuda"), const)
+    assert dev.is_cuda and np.array_equal(dev.cpu().numpy(), ref)
+
+
+def test_hard_bits_agree_with_llr_signs():
+    """Detector decisions -> Gray bits equal the signs of the bit LLRs of the
+    same x-hat (bit 1 <=> LLR < 0), end to end through pipeline.detect."""
+    from oracle import dbp_oracle as O
+
+    const = dbp.make_constellation("qam16")
+    rng = np.random.default_rng(8)
+    n, T, b, u = 40, 14, 64, 8
+    H = (rng.standard_normal((n, b, u)) + 1j * rng.standard_normal((n, b, u))) / np.sqrt(2 * b)
+    s = const.symbols[rng.integers(0, const.size, (n, T, u))]
+    Y = np.einsum("nbu,ntu->ntb", H, s) + 0.1 * (rng.standard_normal((n, T, b)) + 1j * rng.standard_normal((n, T, b)))
+    det = dbp.detect("pd", "lmmse", H, Y, 0.02, [32, 32], const)
+    bits = dbp.gray_bits(det.decisions, const)
+    llr = dbp.llr(det.xhat, det.sigma2, const)
+    assert np.array_equal(np.asarray(bits), (np.asarray(llr) < 0).astype(np.uint8))
+    assert O.gray_labels(const.symbols, const.pam_levels).shape == (const.size,)
