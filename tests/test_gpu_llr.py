@@ -75,3 +75,26 @@ def test_hard_bits_agree_with_llr_signs():
     llr = dbp.llr(det.xhat, det.sigma2, const)
     assert np.array_equal(np.asarray(bits), (np.asarray(llr) < 0).astype(np.uint8))
     assert O.gray_labels(const.symbols, const.pam_levels).shape == (const.size,)
+
+
+def test_lama_soft_outputs_per_symbol_variance():
+    """LAMA reports sigma2 per OFDM symbol ([n][T]); the LLRs of its x-hat with
+    that variance equal the oracle's and their signs give the Gray bits of the
+    detector's own decisions."""
+    from oracle import dbp_oracle as O
+
+    const = dbp.make_constellation("qam16")
+    rng = np.random.default_rng(12)
+    n, T, b, u = 30, 14, 64, 8
+    H = (rng.standard_normal((n, b, u)) + 1j * rng.standard_normal((n, b, u))) / np.sqrt(2 * b)
+    s = const.symbols[rng.integers(0, const.size, (n, T, u))]
+    Y = np.einsum("nbu,ntu->ntb", H, s) + 0.15 * (rng.standard_normal((n, T, b)) + 1j * rng.standard_normal((n, T, b)))
+    det = dbp.detect("pd", "lama", H, Y, 0.045, [32, 32], const, lama_params={"t_max": 6})
+    s2 = np.asarray(det.sigma2)
+    assert s2.shape == (n, T)
+    x = np.asarray(det.xhat)
+    got = dbp.llr(x, s2, const, exact=True)
+    ref = O.bit_llr(x, s2[:, :, None], const.symbols, const.pam_levels, exact=True)
+    assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)) < 1e-4
+    bits = dbp.gray_bits(det.decisions, const)
+    assert np.array_equal(np.asarray(bits), (dbp.llr(x, s2, const) < 0).astype(np.uint8))
