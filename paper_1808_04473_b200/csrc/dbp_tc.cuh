@@ -49,7 +49,10 @@ constexpr int TC_FIRST_CONV = 1 + TC_MMA_W;
 constexpr int TC_FIRST_ASM = TC_FIRST_CONV + TC_CONV_W;
 constexpr int TC_FIRST_SOLVER = TC_FIRST_ASM + TC_ASM_W;
 constexpr int TC_MAX_SOLV = 6;
-constexpr int TC_NOP = 2;  // operand tile ring depth (converter -> MMA)
+#ifndef DBP_TC_NOP
+#define DBP_TC_NOP 2
+#endif
+constexpr int TC_NOP = DBP_TC_NOP;  // operand tile ring depth (converter -> MMA)
 constexpr int TC_CONV = 128;  // threads of one converter set (barrier arrival count)
 constexpr int TC_ASM = 32 * TC_ASM_W;
 constexpr int TC_MAX_THREADS = 32 * (TC_FIRST_SOLVER + TC_MAX_SOLV);

@@ -77,6 +77,8 @@ int main() {
   const V vs[] = {
       {61440, 2, 2, 2, 1}, {61440, 2, 3, 2, 1}, {30720, 2, 2, 2, 1}, {30720, 2, 3, 2, 1}, {30720, 2, 4, 2, 1},
       {30720, 2, 6, 2, 1}, {45056, 2, 2, 2, 1}, {45056, 2, 4, 2, 1}, {92160, 2, 2, 2, 1}, {15360, 2, 8, 2, 1},
+      // cfg2 stage geometry: 2 items (H 2 x 16 KB) + 28 Y rows of 1 KB = 30 copies of ~2 KB
+      {61440, 30, 2, 32, 1}, {61440, 60, 2, 32, 1}, {61440, 15, 2, 32, 1}, {30720, 15, 3, 32, 1},
   };
   for (const V& v : vs) {
     Cfg c{src, total / v.item, v.item, v.split, v.stages, v.lanes, v.contig};
