@@ -352,9 +352,11 @@ def single_gpu(args, wl, name):
                 h, y = copies[k % len(copies)]
                 det.run(h, y, 0.0, n0_dev, W)
             torch.cuda.synchronize()
-    launches = args.steps
     kernel_id = _lib.lib().dbp_last_kernel()
     up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
+    # U = 64 PD on the tensor cores: statistics launch (wide layout) + solve launch
+    two_pass = kernel_id == 2 and up == 64
+    launches = args.steps * (2 if two_pass else 1)
     ms = elapsed_ms / args.steps
     bits = bits_per_step(wl)
     value = bits / (ms * 1e-3) / 1e9
@@ -430,7 +432,9 @@ def single_gpu(args, wl, name):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": (f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (tensor cores, 1 launch/step)"
+                     "kernel": ("dbp::tc_kernel<64, stats> (tensor cores, wide layout) + dbp::stats_kernel<64> "
+                                "(solves), 2 launches/step" if two_pass else
+                                f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (tensor cores, 1 launch/step)"
                                 if kernel_id == 2 else
                                 f"dbp::stream_kernel<{up}> (FP32 SIMT, 1 launch/step)")},
         "cpu_baseline": cpu,

@@ -395,7 +395,11 @@ template <int UP>
 static int launch_tc(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  if (2 * UP + 32 > 128) return fail(DBP_E_UNSUPPORTED, "2U + 32 > 128 rows on the tensor-core path");
+  // U = 64 ("wide": A = the 128 H features, B = [H | Y], N = 160) computes
+  // statistics only; its solves run in stats_kernel (dispatch_stream)
+  constexpr bool WIDE = UP > 32;
+  if (WIDE && p.arch != ARCH_STATS) return 1;
+  if (!WIDE && 2 * UP + 32 > 128) return fail(DBP_E_UNSUPPORTED, "2U + 32 > 128 rows on the tensor-core path");
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -415,6 +419,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   p.pair = (tc_yrow0(UP, 2) + 2 * 32 <= 128) ? 2 : 1;
   if (upi > 1 && (upi & 1)) p.pair = 1;
   if (const char* e = getenv("DBP_TC_PAIR")) p.pair = std::max(1, std::min(2, atoi(e)));
+  if (WIDE) p.pair = 1;
   // staging plan: whole items (several per stage when small) or row blocks
   const int hrow = p.us * 8, yrow = p.T * 8;  // bytes per antenna row of H / Y
   const int item_bytes = p.B * (hrow + yrow);
@@ -501,7 +506,7 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
   if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(2, std::min(TC_MAX_SOLV, atoi(e)));
   while (nsolv > 4 && !fits(p.NS, nsolv)) --nsolv;
   while (p.NS > 2 && !fits(p.NS, nsolv)) --p.NS;
-  while (nsolv > 2 && !fits(p.NS, nsolv)) --nsolv;
+  while (nsolv > (WIDE ? 1 : 2) && !fits(p.NS, nsolv)) --nsolv;  // wide: one statistics writer suffices
   if (fits(p.NS, nsolv)) break;
   if (attempt == 6 || smax < 8 * 1024) return 1;  // does not fit: caller falls back to the SIMT kernel
   smax = smax * 3 / 4;
@@ -513,9 +518,11 @@ static int launch_tc(EqParams& p, cudaStream_t st) {
     if (!p.fd_scratch) return fail(DBP_E_CUDA, "FD scratch allocation failed");
   }
   const bool fdm = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  auto kern = (p.arch == ARCH_STATS) ? tc_kernel<UP, TC_STATS>
-              : fdm ? (lama ? tc_kernel<UP, TC_FD_LAMA> : tc_kernel<UP, TC_FD_LIN>)
-                    : (lama ? tc_kernel<UP, TC_PD_LAMA> : tc_kernel<UP, TC_PD_LIN>);
+  void (*kern)(EqParams, int) = tc_kernel<UP, TC_STATS>;
+  if constexpr (!WIDE)
+    kern = (p.arch == ARCH_STATS) ? tc_kernel<UP, TC_STATS>
+           : fdm ? (lama ? tc_kernel<UP, TC_FD_LAMA> : tc_kernel<UP, TC_FD_LIN>)
+                 : (lama ? tc_kernel<UP, TC_PD_LAMA> : tc_kernel<UP, TC_PD_LIN>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
@@ -574,6 +581,8 @@ static int launch_stats(EqParams& p, cudaStream_t st) {
 
 // U <= 32 -> tensor-core kernel; U = 64 -> SIMT kernel (2(U+T) > 128).
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
+static int dispatch_stats(EqParams& p, cudaStream_t st);
+
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
   p.g_hermitian = 1;  // the streaming kernels build G themselves (full Hermitian matrix)
   const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
@@ -594,6 +603,34 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     if (rc == 0) g_last_kernel = 2;
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
     p.NS = up <= 16 ? 4 : 3;
+  }
+  // U = 64: statistics {G, y_mrc} on the tensor cores (wide layout); PD
+  // linear equalization then runs its solves in stats_kernel on them
+  const bool wide_ok = !force_simt && up == 64 && !getenv("DBP_NO_WIDE") &&
+                       (p.arch == ARCH_STATS || (p.arch == ARCH_PD && p.kind != EQ_LAMA));
+  if (wide_ok) {
+    if (p.arch == ARCH_STATS) {
+      const int rc = launch_tc<64>(p, st);
+      if (rc == 0) g_last_kernel = 2;
+      if (rc <= 0) return rc;
+    } else {
+      EqParams q = p;
+      q.arch = ARCH_STATS;
+      q.sum_clusters = 1;
+      const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
+      q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
+      if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
+      const int rc = launch_tc<64>(q, st);
+      if (rc < 0) return rc;
+      if (rc == 0) {
+        g_last_kernel = 2;
+        EqParams r = p;
+        r.stats_in = q.stats_out;
+        r.C = 1;
+        return dispatch_stats(r, st);
+      }
+    }
+    p.NS = 3;
   }
   g_last_kernel = 1;
   switch (up) {

@@ -93,7 +93,9 @@ __host__ __device__ inline TcLayout make_tc_layout(int UP, int TP, int sbytes, i
   o = align_up(o, 1024);
   L.ops = o;
   L.lbo = (KC / 8) * 1024;  // one 32-row M block of a K=KC tile
-  L.opb = 4 * L.lbo;        // 4 M blocks = the 128 rows one MMA reads
+  // 4 M blocks = the 128 rows one MMA reads; wide (U = 64): 5 blocks, the
+  // 128 H features (A) and the Y block after them (B = all 160 rows)
+  L.opb = (UP > 32 ? 5 : 4) * L.lbo;
   o += 2 * TC_NOP * L.opb;  // [hi0][lo0][hi1][lo1]...
   L.work = o;
   L.w = make_work_layout(0, UP, TP, C, lama, false);
@@ -288,9 +290,14 @@ enum { TC_STATS = 0, TC_PD_LIN = 1, TC_PD_LAMA = 2, TC_FD_LIN = 3, TC_FD_LAMA = 
 template <int UP, int MODE>
 __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_constant__ EqParams p, int nsolv) {
   extern __shared__ __align__(1024) char smem[];
-  const int pair = p.pair;
-  const int N = pair * 2 * UP;  // MMA N: the H features of both halves
-  constexpr int SW = 2 * 2 * UP;  // TMEM columns per accumulator slot (room for pair == 2)
+  // wide (U = 64, statistics only): the 2U = 128 H features fill M, so the Y
+  // block moves to N: A = tile rows [0, 128) (H), B = rows [0, 160) ([H | Y])
+  // of the same operand tile; accumulator lane = H feature, columns = [H | Y]
+  constexpr bool WIDE = UP > 32;
+  static_assert(!WIDE || MODE == 0, "the wide layout only produces statistics");
+  const int pair = WIDE ? 1 : p.pair;
+  const int N = WIDE ? 2 * UP + 32 : pair * 2 * UP;  // MMA N
+  constexpr int SW = WIDE ? 2 * UP + 32 : 2 * 2 * UP;  // TMEM columns per accumulator slot (room for pair == 2)
   // accumulators: 2 buffers (pairs v, v+1) x TC_MMA_W partial sums (one per
   // MMA issuer warp), column (2 a + m) * SW
   constexpr int TCOLS = 2 * TC_MMA_W * SW;
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) +
                                (uint32_t)((TC_MMA_W * a + (cpu_mma == 1 ? (v * cpu) % TC_MMA_W : 0)) * SW);
         const int rloc = is_h ? (m - hh * 2 * UP) : ((m - YB) & 31);  // row within the half
-        for (int c16 = 0; c16 < pair * 2 * UP / 16; ++c16) {
+        for (int c16 = 0; c16 < (WIDE ? SW : pair * 2 * UP) / 16; ++c16) {
           float vv[16];
           tmem_ld16(taddr + 16 * c16, vv);
           for (int mm = 1; mm < cpu_mma; ++mm) {
@@ -774,6 +781,20 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           }
           const int colbase = 8 * c16 - hh * UP;  // UE column of vv[0] within this row's half
           const bool mine = write && colbase >= 0 && colbase < UP;
+          if (WIDE && colbase >= UP) {
+            // Y columns (symbol t = colbase - UP + c): y_t[u] for this lane's
+            // UE u, same re/im recombination as G (rows are H features here)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float po = __shfl_xor_sync(0xffffffffu, vv[2 * c + 1], 1);
+              const int t = colbase - UP + c;
+              if (write && t < T) {
+                const float val = odd ? (po - vv[2 * c]) : (vv[2 * c] + po);
+                Zf[(t * LD + (rloc >> 1)) * 2 + (odd ? 1 : 0)] = val;
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const float po = __shfl_xor_sync(0xffffffffu, vv[2 * c + 1], 1);

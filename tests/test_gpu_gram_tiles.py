@@ -4,7 +4,8 @@ numpy restatement of the per-cluster products G_c = H_c^H H_c, z_c = H_c^H y
 exercise the operand-tile layouts: two units paired per tcgen05.mma (a warp
 then holds accumulator rows of both units, e.g. Y rows of unit 0 and 1), a
 single unit per tile, per-cluster and cluster-summed outputs, odd and tiny
-T, U=8/16/32 and U=64 (SIMT path)."""
+T, U=8/16/32, and U=64 on the wide layout (A = the 128 H features, B = [H | Y],
+N = 160), including ragged row chunks and u < 64."""
 
 import numpy as np
 import pytest
@@ -29,6 +30,11 @@ CASES = [
     (3, 128, 32, 14, [0, 64, 128], 0),
     (2, 128, 64, 7, [0, 64, 128], 0),
     (7, 96, 16, 3, [0, 32, 64, 96], 1),
+    # wide (U = 64): cfg5 geometry summed, one cluster, ragged clusters (SIMT), u < UP, T = 16
+    (3, 512, 64, 14, list(range(0, 513, 64)), 1),
+    (2, 64, 64, 16, [0, 64], 1),
+    (3, 80, 64, 14, [0, 48, 80], 0),
+    (2, 256, 62, 5, [0, 128, 256], 1),
 ]
 
 
@@ -57,3 +63,5 @@ def test_gram_mrc_tiles(n, b, u, t, offs, summed):
             # 3xTF32 / fp32 accumulation: ~1e-6 relative to the largest entry
             assert np.abs(o[i, k, :u * u].reshape(u, u) - G).max() < 2e-5 * scale_g, (i, k, "G")
             assert np.abs(o[i, k, u * u:].reshape(t, u) - Z).max() < 2e-5 * scale_z, (i, k, "Z")
+    if len(set(np.diff(offs))) == 1:  # uniform clusters run on the tensor cores (ragged: SIMT kernel)
+        assert _lib.lib().dbp_last_kernel() == 2
