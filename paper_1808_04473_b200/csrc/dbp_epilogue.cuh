@@ -324,7 +324,6 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     m[r] = v;
   }
   for (int k0 = 0; k0 < UP; k0 += RS) {
-    const int rot = k0 / RS;  // rotations done so far
     for (int kk = 0; kk < RS && k0 + kk < UP; ++kk) {
       const int k = k0 + kk;
       float2* rk = rowb + (k & 1) * UP;
@@ -332,8 +331,15 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
       if (live) {
         if (i0 == kk) rk[j] = m[0];
         if (j == k) {
+          // slot = register index: readers with the same i0 share the writer's
+          // rotation state, so register r of every such thread holds the same row
+          if constexpr (EPT >= 2) {
 #pragma unroll
-          for (int r = 0; r < EPT; ++r) ck[i0 * EPT + ((r + rot) & (EPT - 1))] = m[r];
+            for (int r = 0; r < EPT; r += 2)
+              *reinterpret_cast<float4*>(ck + i0 * EPT + r) = make_float4(m[r].x, m[r].y, m[r + 1].x, m[r + 1].y);
+          } else {
+            ck[i0] = m[0];
+          }
         }
       }
       tm.sync();
@@ -343,14 +349,21 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
         p = 1.f;
       }
       if (k >= u) p = 1.f;  // padded step: identity pivot
-      const float rp = 1.f / p;
+      const float rp = __frcp_rn(p);  // = 1.f / p (correctly rounded), no division slow path
       if (live) {
         const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rk[j], rp);
+        if constexpr (EPT >= 2) {
 #pragma unroll
-        for (int r = 0; r < EPT; ++r) {
-          float2 ci = ck[i0 * EPT + ((r + rot) & (EPT - 1))];
-          if (r == 0 && i0 == kk) ci = make_float2(p - 1.f, 0.f);
-          c_fms(m[r], ci, rj);
+          for (int r = 0; r < EPT; r += 2) {
+            const float4 c2 = *reinterpret_cast<const float4*>(ck + i0 * EPT + r);
+            float2 ci = make_float2(c2.x, c2.y);
+            if (r == 0 && i0 == kk) ci = make_float2(p - 1.f, 0.f);
+            c_fms(m[r], ci, rj);
+            c_fms(m[r + 1], make_float2(c2.z, c2.w), rj);
+          }
+        } else {
+          const float2 ci = (i0 == kk) ? make_float2(p - 1.f, 0.f) : ck[i0];
+          c_fms(m[0], ci, rj);
         }
       }
     }

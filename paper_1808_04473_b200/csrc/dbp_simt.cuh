@@ -330,8 +330,18 @@ __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqPar
   for (int64_t n = blockIdx.x; n < p.n_items; n += gridDim.x) {
     reset_flags(w, tm);
     const float2* src = p.stats_in + n * rec;
-    for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
-    for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
+    if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_in) & 15)) {  // float4 pairs, shifts instead of divisions
+      constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
+      const float4* s4 = reinterpret_cast<const float4*>(src);  // rec is even: 16-byte aligned
+      for (int e = tid; e < (UP * UP + T * UP) / 2; e += NT) {
+        const int r = e >> SH, c = 2 * (e & (UP / 2 - 1));
+        float2* dst = (r < UP) ? w.G + r * w.LD + c : w.Z + (r - UP) * w.LD + c;
+        *reinterpret_cast<float4*>(dst) = s4[e];
+      }
+    } else {
+      for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
+      for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
+    }
     __syncthreads();
     unit_epilogue<UP>(w, p, n, 0, true, cl_first, tm);
     __syncthreads();
