@@ -605,7 +605,10 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     p.NS = up <= 16 ? 4 : 3;
   }
   // U = 64: statistics {G, y_mrc} on the tensor cores (wide layout); PD
-  // linear equalization then runs its solves in stats_kernel on them
+  // linear equalization then runs its solves in stats_kernel on them.  Not
+  // FD: its per-cluster Grams (B_c = U = 64 at cfg5) are ill-conditioned, and
+  // 3xTF32 (no lo.lo term) left FD-ZF 5e-3 from the float64 reference where
+  // the FP32 SIMT Gram stays at 2e-4 (cfg5a, measured), for a 2 % gain.
   const bool wide_ok = !force_simt && up == 64 && !getenv("DBP_NO_WIDE") &&
                        (p.arch == ARCH_STATS || (p.arch == ARCH_PD && p.kind != EQ_LAMA));
   if (wide_ok) {

@@ -32,6 +32,7 @@ CASES = [
     (7, 96, 16, 3, [0, 32, 64, 96], 1),
     # wide (U = 64): cfg5 geometry summed, one cluster, ragged clusters (SIMT), u < UP, T = 16
     (3, 512, 64, 14, list(range(0, 513, 64)), 1),
+    (2, 512, 64, 14, list(range(0, 513, 64)), 0),
     (2, 64, 64, 16, [0, 64], 1),
     (3, 80, 64, 14, [0, 48, 80], 0),
     (2, 256, 62, 5, [0, 128, 256], 1),
