@@ -691,8 +691,20 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
     const int ncl = p.sum_clusters ? 1 : p.C;
     const int cl = p.sum_clusters ? 0 : cluster;
     float2* dst = p.stats_out + ((size_t)n * ncl + cl) * (size_t)(u * u + T * u);
-    for (int e = tid; e < u * u; e += NT) dst[e] = w.G[(e / u) * LD + (e % u)];
-    for (int e = tid; e < T * u; e += NT) dst[u * u + e] = w.Z[(e / u) * LD + (e % u)];
+    if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_out) & 15)) {
+      // rows of UP complex as float4 pairs, shifts instead of divisions (a
+      // lone writer warp moves 40 KB per unit at U = 64)
+      constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
+      float4* d4 = reinterpret_cast<float4*>(dst);  // record length even: 16-byte aligned
+      for (int e = tid; e < (UP * UP + T * UP) / 2; e += NT) {
+        const int r = e >> SH, c = 2 * (e & (UP / 2 - 1));
+        const float2* src = (r < UP) ? w.G + r * LD + c : w.Z + (r - UP) * LD + c;
+        d4[e] = *reinterpret_cast<const float4*>(src);
+      }
+    } else {
+      for (int e = tid; e < u * u; e += NT) dst[e] = w.G[(e / u) * LD + (e % u)];
+      for (int e = tid; e < T * u; e += NT) dst[u * u + e] = w.Z[(e / u) * LD + (e % u)];
+    }
     tm.sync();
     return;
   }
