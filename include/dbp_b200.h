@@ -200,6 +200,16 @@ int dbp_llr(const void* xhat, const float* sigma2, int64_t n, int T, int u, int 
  * idx_bytes = 1, int32 hard_detect indices when 4); label as in dbp_llr. */
 int dbp_gray_bits(const void* idx, int idx_bytes, int64_t n, int L, uint8_t* bits, void* stream);
 
+/* Gauss-Hermite quadratures of the large-system analysis (SURVEY.md 8(f)
+ * rank 4; replaces kernels.lama_mse_pam / lama_mse / mi_awgn,
+ * _kernels.pyx:74-158), fp64, one value per point x[n] (device): kind 0 =
+ * PAM posterior-mean MSE (values = M real levels), 1 = 2-D MSE, 2 = AWGN
+ * mutual information in bits (values = M complex symbols interleaved re/im,
+ * host); x = sigma^2 (MSE) or the noise variance (MI); nodes / weights = the
+ * q-point rule for exp(-x^2) (device); out[n] (device). */
+int dbp_quadrature(int kind, const double* x, int64_t n, const double* values, int M, const double* nodes,
+                   const double* weights, int q, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

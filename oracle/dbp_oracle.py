@@ -406,3 +406,63 @@ def bit_llr(x, s2, symbols, levels, exact=False):
             out[..., b] += (np.log(np.exp(m0[..., None] - d0).sum(-1))
                             - np.log(np.exp(m1[..., None] - d1).sum(-1)))
     return out
+
+
+# --------------------------------------------------------------------------
+# Gauss-Hermite quadratures of the large-system analysis (SURVEY.md 8(f)
+# rank 4): _kernels.pyx:74-158 / _kernels_py.py:31-77, nodes and weights of
+# kernels.gauss_hermite (kernels.py:34-38, scipy's roots_hermite: numpy's
+# hermgauss returns NaN at the default PAM order 2048).  Pinned by tests/golden/golden_quad.npz, made by
+# running the reference's own kernels (tests/golden/make_golden_quad.py).
+# --------------------------------------------------------------------------
+def gauss_hermite(order):
+    """kernels.py:34-38: nodes/weights for the weight exp(-x^2)."""
+    from scipy.special import roots_hermite
+
+    return roots_hermite(order)
+
+
+def _post_mean_pam(x, levels, sigma2):
+    d2 = (x[..., None] - levels) ** 2
+    d2 = d2 - d2.min(axis=-1, keepdims=True)
+    w = np.exp(-d2 / sigma2)
+    return (w @ levels) / w.sum(axis=-1)
+
+
+def lama_mse_pam(sigma2, levels, order=2048):
+    """_kernels.pyx:99-126: twice the 1-D posterior-mean MSE of the PAM set."""
+    nodes, weights = gauss_hermite(order)
+    levels = np.asarray(levels, dtype=float)
+    x = levels[:, None] + np.sqrt(sigma2) * nodes[None, :]  # [a][j]
+    f = _post_mean_pam(x, levels, sigma2)
+    total = np.sum(weights[None, :] * (f - levels[:, None]) ** 2)
+    return 2.0 * total / (levels.size * np.sqrt(np.pi))
+
+
+def lama_mse(sigma2, symbols, order=32):
+    """_kernels.pyx:74-96: 2-D posterior-mean MSE over the symbol set."""
+    nodes, weights = gauss_hermite(order)
+    symbols = np.asarray(symbols, dtype=np.complex128)
+    noise = np.sqrt(sigma2) * (nodes[:, None] + 1j * nodes[None, :])
+    w2 = weights[:, None] * weights[None, :]
+    total = 0.0
+    for s in symbols:
+        f, _ = posterior_mean_var((s + noise).ravel(), sigma2, symbols)
+        total += float(np.sum(w2.ravel() * np.abs(f - s) ** 2))
+    return total / (symbols.size * np.pi)
+
+
+def mi_awgn(noise_var, symbols, order=32):
+    """_kernels.pyx:129-158: mutual information (bits) of the uniform input
+    over complex AWGN, log-sum-exp stabilised."""
+    nodes, weights = gauss_hermite(order)
+    symbols = np.asarray(symbols, dtype=np.complex128)
+    noise = (np.sqrt(noise_var) * (nodes[:, None] + 1j * nodes[None, :])).ravel()
+    w2 = (weights[:, None] * weights[None, :]).ravel()
+    penalty = 0.0
+    for a in symbols:
+        e = -(np.abs(a - symbols[None, :] + noise[:, None]) ** 2 - (np.abs(noise) ** 2)[:, None]) / noise_var
+        emax = e.max(axis=1)
+        lse = emax + np.log(np.sum(np.exp(e - emax[:, None]), axis=1))
+        penalty += float(np.sum(w2 * lse)) / np.log(2.0)
+    return np.log2(symbols.size) - penalty / (symbols.size * np.pi)

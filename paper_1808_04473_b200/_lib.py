@@ -48,6 +48,7 @@ SIGNATURES = {
     "dbp_fuse_estimates": [_vp, _vp, _vp, _i, _i64, _vp, _vp, _vp],
     "dbp_llr": [_vp, _vp, _i64, _i, _i, _i, _vp, _i, _i, _vp, _vp],
     "dbp_gray_bits": [_vp, _i, _i64, _i, _vp, _vp],
+    "dbp_quadrature": [_i, _vp, _i64, _vp, _i, _vp, _vp, _i, _vp, _vp],
     "dbp_synthesize": [C.c_uint64, _i64, _i64, _i, _i, _i, _vp, _i, _f, _vp, _i64, _vp, _vp, _vp, _vp],
 }
 

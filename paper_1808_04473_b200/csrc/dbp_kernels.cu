@@ -200,6 +200,104 @@ __global__ void gray_bits_kernel(const IDX* __restrict__ idx, int64_t n, int h, 
   }
 }
 
+// Gauss-Hermite quadratures of the large-system analysis (SURVEY.md 8(f)
+// rank 4; _kernels.pyx:74-158), fp64 like the reference: one CTA per
+// evaluation point, the (symbol, node[, node]) terms strided over its
+// threads, a fixed-order tree reduction (deterministic).
+//   QK_MSE_PAM: 2/(L sqrt(pi)) sum_a sum_j w_j (F(a + s n_j) - a)^2
+//   QK_MSE_2D : 1/(M pi) sum_s sum_jk w_j w_k |F(s + s(n_j + i n_k)) - s|^2
+//   QK_MI     : log2 M - 1/(M pi ln 2) sum_a sum_jk w_j w_k lse_b(e_b)
+// F = posterior mean of the uniform prior at noise variance x (= sigma^2).
+enum { QK_MSE_PAM = 0, QK_MSE_2D = 1, QK_MI = 2 };
+struct QuadSet {
+  int M;  // symbols (2-D kinds) or levels (PAM)
+  double re[MAX_SYMS], im[MAX_SYMS];
+};
+constexpr int QUAD_THREADS = 256;
+
+__global__ void __launch_bounds__(QUAD_THREADS) quad_kernel(int kind, const double* __restrict__ xs,
+                                                            const __grid_constant__ QuadSet qs,
+                                                            const double* __restrict__ nodes,
+                                                            const double* __restrict__ weights, int q,
+                                                            double* __restrict__ out) {
+  __shared__ double red[QUAD_THREADS];
+  const double x = xs[blockIdx.x];
+  const double sigma = sqrt(x);
+  const int M = qs.M;
+  double acc = 0.0;
+  if (kind == QK_MSE_PAM) {
+    for (int t = threadIdx.x; t < M * q; t += QUAD_THREADS) {
+      const int a = t / q, j = t - a * q;
+      const double v = qs.re[a] + sigma * nodes[j];
+      double dmin = 1e300;
+      for (int k = 0; k < M; ++k) {
+        const double d = v - qs.re[k];
+        dmin = fmin(dmin, d * d);
+      }
+      double ws = 0.0, f = 0.0;
+      for (int k = 0; k < M; ++k) {
+        const double d = v - qs.re[k];
+        const double w = exp(-(d * d - dmin) / x);
+        ws += w;
+        f += w * qs.re[k];
+      }
+      f /= ws;
+      acc += weights[j] * (f - qs.re[a]) * (f - qs.re[a]);
+    }
+  } else {
+    for (int t = threadIdx.x; t < M * q * q; t += QUAD_THREADS) {
+      const int a = t / (q * q), r = t - a * q * q, j = r / q, k = r - j * q;
+      const double nr = sigma * nodes[j], ni = sigma * nodes[k];
+      const double wjk = weights[j] * weights[k];
+      if (kind == QK_MSE_2D) {
+        const double zr = qs.re[a] + nr, zi = qs.im[a] + ni;
+        double dmin = 1e300;
+        for (int b = 0; b < M; ++b) {
+          const double dr = zr - qs.re[b], di = zi - qs.im[b];
+          dmin = fmin(dmin, dr * dr + di * di);
+        }
+        double ws = 0.0, fr = 0.0, fi = 0.0;
+        for (int b = 0; b < M; ++b) {
+          const double dr = zr - qs.re[b], di = zi - qs.im[b];
+          const double w = exp(-((dr * dr + di * di) - dmin) / x);
+          ws += w;
+          fr += w * qs.re[b];
+          fi += w * qs.im[b];
+        }
+        const double er = fr / ws - qs.re[a], ei = fi / ws - qs.im[a];
+        acc += wjk * (er * er + ei * ei);
+      } else {  // QK_MI
+        const double n2 = nr * nr + ni * ni;
+        double emax = -1e300;
+        for (int b = 0; b < M; ++b) {
+          const double dr = qs.re[a] - qs.re[b] + nr, di = qs.im[a] - qs.im[b] + ni;
+          emax = fmax(emax, -((dr * dr + di * di) - n2) / x);
+        }
+        double lse = 0.0;
+        for (int b = 0; b < M; ++b) {
+          const double dr = qs.re[a] - qs.re[b] + nr, di = qs.im[a] - qs.im[b] + ni;
+          lse += exp(-((dr * dr + di * di) - n2) / x - emax);
+        }
+        acc += wjk * (emax + log(lse));
+      }
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = QUAD_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double pi = 3.141592653589793, tot = red[0];
+    double r;
+    if (kind == QK_MSE_PAM) r = 2.0 * tot / (M * sqrt(pi));
+    else if (kind == QK_MSE_2D) r = tot / (M * pi);
+    else r = log2((double)M) - tot / (M * pi * log(2.0));
+    out[blockIdx.x] = r;
+  }
+}
+
 // ---- small element-wise kernels behind the per-vector drop-in API --------
 // fuse_partials (equalize.py:96-107): out = sum_p parts[p]
 __global__ void stats_sum_kernel(const float2* __restrict__ parts, int P, int64_t count, float2* out) {
@@ -979,6 +1077,34 @@ int dbp_gray_bits(const void* idx, int idx_bytes, int64_t n, int L, uint8_t* bit
   else
     gray_bits_kernel<<<grid_for(n), 256, 0, cs>>>(static_cast<const int32_t*>(idx), n, h, bits);
   return cuda_check("gray_bits_kernel");
+}
+
+// Gauss-Hermite quadratures at n points x (device,
+// fp64): kind 0 = lama_mse_pam (values = M real levels), 1 = lama_mse,
+// 2 = mi_awgn (values = M complex symbols, interleaved re/im; host); nodes /
+// weights: q-point rule for exp(-x^2) (device).
+int dbp_quadrature(int kind, const double* x, int64_t n, const double* values, int M, const double* nodes,
+                   const double* weights, int q, double* out, void* stream) {
+  if (n <= 0) return DBP_OK;
+  if (!x || !values || !nodes || !weights || !out) return fail(DBP_E_ARG, "null pointer");
+  if (kind < QK_MSE_PAM || kind > QK_MI) return fail(DBP_E_ARG, "unknown quadrature kind");
+  if (M < 1 || M > MAX_SYMS || q < 1) return fail(DBP_E_ARG, "bad set size or order");
+  if ((int64_t)M * q * (kind == QK_MSE_PAM ? 1 : q) > (int64_t)1 << 30) return fail(DBP_E_UNSUPPORTED, "order too large");
+  if (n > 0x7fffffff) return fail(DBP_E_UNSUPPORTED, "too many points");
+  QuadSet qs;
+  memset(&qs, 0, sizeof(qs));
+  qs.M = M;
+  for (int k = 0; k < M; ++k) {
+    if (kind == QK_MSE_PAM) {
+      qs.re[k] = values[k];
+    } else {
+      qs.re[k] = values[2 * k];
+      qs.im[k] = values[2 * k + 1];
+    }
+  }
+  quad_kernel<<<(unsigned)n, QUAD_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(kind, x, qs, nodes, weights, q,
+                                                                                  out);
+  return cuda_check("quad_kernel");
 }
 
 }  // extern "C"

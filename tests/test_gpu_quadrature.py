@@ -1,0 +1,58 @@
+"""dbp_quadrature (paper_1808_04473_b200.asymptotics)
+against the reference's own quadratures and analysis functions
+(tests/golden/golden_quad.npz from tests/golden/make_golden_quad.py) and the
+oracle restatement: fp64 on the GPU, agreement to ~1e-11 relative."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1808_04473_b200 as dbp
+from oracle import dbp_oracle as O
+from paper_1808_04473_b200 import asymptotics as A
+
+pytestmark = pytest.mark.gpu
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_quad.npz"))
+
+
+def close(a, b, rtol=1e-10, atol=1e-15):
+    np.testing.assert_allclose(a, b, rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("name", ["qpsk", "qam16", "qam64"])
+def test_quadratures_match_reference(name):
+    c = dbp.make_constellation(name)
+    s2 = G["sigma2"]
+    close(A.lama_mse_pam(s2, c.pam_levels), G[f"{name}_mse_pam"])  # one launch, 6 points
+    close(A.lama_mse_pam(s2, c.pam_levels, 64), G[f"{name}_mse_pam_o64"])
+    close(A.lama_mse(s2, c.symbols, 16), G[f"{name}_mse_2d_o16"])
+    close(A.mi_awgn(c.es / G["sinr"][1:], c.symbols, 16), G[f"{name}_mi_o16"])
+    close(A.awgn_mutual_information(c, G["sinr"], order=16), G[f"{name}_awgn_mi"])
+    spec = A.MseSpec("lama", es=c.es, constellation=c)
+    close(A.psi_mse(spec, s2), G[f"{name}_psi_lama"])
+    close(A.se_trajectory(c, 0.05, 0.5, 8), G[f"{name}_se_traj"])
+    # scalar calls keep the reference's scalar return type
+    assert isinstance(A.lama_mse_pam(0.1, c.pam_levels), float)
+
+
+def test_closed_form_psi_and_errors():
+    for kind in ("mrc", "zf", "lmmse"):
+        close(A.psi_mse(A.MseSpec(kind), G["sigma2"]), G[f"psi_{kind}"], rtol=1e-15)
+    with pytest.raises(dbp.ConfigError):
+        A.psi_mse(A.MseSpec("zf"), 0.0)
+    with pytest.raises(dbp.ConfigError):
+        A.MseSpec("lama")
+    with pytest.raises(dbp.ConfigError):
+        A.awgn_mutual_information(dbp.make_constellation("qpsk"), -1.0)
+
+
+def test_sweep_matches_oracle_and_limits():
+    """A 200-point MI sweep in one launch equals the oracle point by point on a
+    sample; MI rises from 0 to log2 M."""
+    c = dbp.make_constellation("qam16")
+    sinr = np.geomspace(1e-3, 1e3, 200)
+    mi = A.awgn_mutual_information(c, sinr, order=12)
+    assert np.all(np.diff(mi) > -1e-12) and mi[0] < 0.01 and abs(mi[-1] - 4.0) < 1e-6  # saturates at log2 M
+    for i in (0, 57, 133, 199):
+        close(mi[i], O.mi_awgn(c.es / sinr[i], c.symbols, 12), rtol=1e-10)
