@@ -9,9 +9,15 @@ analysis functions built directly on them (asymptotics.py: ``MseSpec``
 defaults (orders 2048 for the factorised PAM rule, 32 for the 2-D rules) and
 errors.  The sums run in fp64 in ``dbp_quadrature`` (one CTA per evaluation
 point); every function also takes an ARRAY of points and evaluates them in
-one launch, which is where the GPU pays (SNR / rate sweeps).  The
-fixed-point, closed-form SINR and rate-search parts of the reference's
-analysis stay out of scope (scalar, ms on the host).
+one launch, which is where the GPU pays (SNR / rate sweeps).
+
+On top of them, the decoupled fixed points and the post-equalization SINRs
+the Monte Carlo driver maps to ``ser_predicted`` (asymptotics.py:75-111,
+132-235, 291-316): ``solve_fixed_point``, ``sinr_pd_closed_form``,
+``sinr_fd``, ``sinr_fd_zf_closed``, ``sinr_fd_lmmse_closed``,
+``asymptotic_sinr`` -- scalar host iterations whose only heavy step, the
+message-passing MSE, is the GPU quadrature.  The rate searches
+(``sinr_for_rate``, ``min_antenna_ratio``) stay out of scope.
 """
 
 from __future__ import annotations
@@ -21,9 +27,12 @@ from functools import lru_cache
 
 import numpy as np
 
+import math
+
 from . import _lib
 from .equalize import Equalizer
-from .errors import ConfigError
+from .errors import ConfigError, InvalidRegimeError, NonConvergenceError
+from .model import Architecture
 
 DEFAULT_QUAD_ORDER = 32  # kernels.py:22
 DEFAULT_PAM_ORDER = 2048  # kernels.py:25
@@ -158,3 +167,142 @@ def awgn_mutual_information(constellation, sinr, order=DEFAULT_QUAD_ORDER):
     if np.any(pos):
         out[pos] = np.atleast_1d(mi_awgn(constellation.es / s[pos], constellation.symbols, order))
     return float(out) if out.ndim == 0 else out
+
+
+_ZF_MARGIN = 1e-9  # asymptotics.py:25 -- ZF needs beta/w < 1 - margin
+
+
+@dataclass
+class FixedPointResult:
+    sigma2: float
+    sinr: float
+    iterations: int
+    converged: bool
+
+
+def solve_fixed_point(spec, n0, beta, w=1.0, tol=1e-12, max_iter=100_000):
+    """asymptotics.py:82-109: largest solution of w sigma2 = N0 + beta
+    Psi(sigma2), iterated down from (N0 + beta Es)/w."""
+    if n0 <= 0:
+        raise ConfigError("fixed point requires N0 > 0")
+    if w <= 0:
+        raise ConfigError("cluster fraction w must be positive")
+    if spec.kind is Equalizer.ZF and beta / w >= 1.0 - _ZF_MARGIN:
+        raise InvalidRegimeError(f"ZF fixed point needs beta/w < 1, got beta={beta}, w={w}")
+    sigma2 = (n0 + beta * spec.es) / w
+    for it in range(1, max_iter + 1):
+        nxt = (n0 + beta * psi_mse(spec, sigma2)) / w
+        if abs(nxt - sigma2) <= tol * sigma2:
+            return FixedPointResult(sigma2=nxt, sinr=spec.es / nxt, iterations=it, converged=True)
+        sigma2 = nxt
+    raise NonConvergenceError(f"fixed point did not converge within {max_iter} iterations "
+                              f"(kind={spec.kind}, beta={beta}, w={w})")
+
+
+def _lmmse_cluster_sinr(g, beta, w):
+    """Per-cluster L-MMSE SINR for an antenna fraction w (asymptotics.py:148-152):
+    the positive root of s^2 + (1 - g (w - beta)) s - g w = 0."""
+    b = 1.0 - g * (w - beta)
+    return 0.5 * (math.sqrt(b * b + 4.0 * g * w) - b)
+
+
+def sinr_pd_closed_form(kind, es_over_n0, beta):
+    """asymptotics.py:132-145: PD (= centralized) SINR of the linear kinds."""
+    kind = Equalizer(kind)
+    g = es_over_n0
+    if kind is Equalizer.MRC:
+        return g / (1.0 + beta * g)
+    if kind is Equalizer.ZF:
+        if beta >= 1.0 - _ZF_MARGIN:
+            raise InvalidRegimeError(f"ZF closed form needs beta < 1, got {beta}")
+        return g * (1.0 - beta)
+    if kind is Equalizer.LMMSE:
+        return _lmmse_cluster_sinr(g, beta, 1.0)
+    raise ConfigError("no closed form for the message-passing equalizer")
+
+
+def _check_weights(weights):
+    w = np.asarray(weights, dtype=float)
+    if w.ndim != 1 or abs(w.sum() - 1.0) > 1e-9 or np.any(w < 0):
+        raise ConfigError(f"invalid cluster weights {weights}")
+    return w
+
+
+@dataclass
+class FdSinrResult:
+    per_cluster_sinr: np.ndarray
+    sinr: float
+    sigma2: float
+
+
+def sinr_fd(spec, es_over_n0, beta, weights, tol=1e-12):
+    """asymptotics.py:161-201: per-cluster fixed points; fused SINR = sum of
+    the cluster SINRs, fused variance their harmonic combination, checked
+    against N0 + beta sum_c nu_c Psi(sigma_c^2)."""
+    weights = _check_weights(weights)
+    n0 = spec.es / es_over_n0
+    if spec.kind is Equalizer.ZF and np.any(beta / weights[weights > 0] >= 1.0 - _ZF_MARGIN):
+        raise InvalidRegimeError("ZF in the FD architecture needs w_c > beta for every cluster")
+    per = np.zeros(weights.size)
+    s2c = np.full(weights.size, np.inf)
+    for i, w in enumerate(weights):
+        if w == 0.0:
+            continue  # an empty cluster carries no information
+        fp = solve_fixed_point(spec, n0, beta, w=w, tol=tol)
+        per[i], s2c[i] = fp.sinr, fp.sigma2
+    total = float(per.sum())
+    if total <= 0:
+        raise InvalidRegimeError("fused SINR is zero; no cluster carries information")
+    sigma2_fd = spec.es / total
+    fin = s2c[np.isfinite(s2c)]
+    nu = (1.0 / fin) / np.sum(1.0 / fin)
+    psi = np.atleast_1d(psi_mse(spec, fin))
+    if abs(n0 + beta * float(np.dot(nu, psi)) - sigma2_fd) > 1e-9 * max(sigma2_fd, 1e-300):
+        raise NonConvergenceError("fused-variance identity violated")
+    return FdSinrResult(per_cluster_sinr=per, sinr=total, sigma2=sigma2_fd)
+
+
+def sinr_fd_zf_closed(es_over_n0, beta, c):
+    """asymptotics.py:204-209: (Es/N0)(1 - C beta)."""
+    if c * beta >= 1.0 - _ZF_MARGIN:
+        raise InvalidRegimeError(f"ZF-FD closed form needs C*beta < 1, got {c * beta}")
+    return es_over_n0 * (1.0 - c * beta)
+
+
+@dataclass
+class LmmseFdSinr:
+    value: float
+    uniform_lower_bound: float
+    pd_upper_bound: float
+
+
+def sinr_fd_lmmse_closed(es_over_n0, beta, weights):
+    """asymptotics.py:219-235: sum of the per-cluster closed forms, with the
+    uniform-allocation lower bound and the PD upper bound."""
+    w = _check_weights(weights)
+    g = es_over_n0
+    value = float(sum(_lmmse_cluster_sinr(g, beta, x) for x in w))
+    lower = w.size * _lmmse_cluster_sinr(g, beta, 1.0 / w.size)
+    return LmmseFdSinr(value=value, uniform_lower_bound=lower,
+                       pd_upper_bound=sinr_pd_closed_form(Equalizer.LMMSE, g, beta))
+
+
+def asymptotic_sinr(kind, architecture, constellation, es_over_n0, beta, weights=None, order=None):
+    """asymptotics.py:291-316: large-system SINR of any (equalizer,
+    architecture) pair."""
+    kind = Equalizer(kind)
+    architecture = Architecture(architecture)
+    if architecture is Architecture.FD and kind is not Equalizer.MRC:
+        if weights is None:
+            raise ConfigError("the FD architecture needs cluster weights")
+        weights = np.asarray(weights, dtype=float)
+        if kind is Equalizer.ZF:
+            return sinr_fd_zf_closed(es_over_n0, beta, weights.size)
+        if kind is Equalizer.LMMSE:
+            return sinr_fd_lmmse_closed(es_over_n0, beta, weights).value
+        spec = MseSpec(Equalizer.LAMA, es=constellation.es, constellation=constellation, order=order)
+        return sinr_fd(spec, es_over_n0, beta, weights).sinr
+    if kind is Equalizer.LAMA:
+        spec = MseSpec(Equalizer.LAMA, es=constellation.es, constellation=constellation, order=order)
+        return solve_fixed_point(spec, constellation.es / es_over_n0, beta).sinr
+    return sinr_pd_closed_form(kind, es_over_n0, beta)

@@ -14,8 +14,9 @@ and shared by every (equalizer, architecture) pair of an experiment set
 own design intends ("experiments that differ only in the equalizer or
 architecture see identical channel, symbol, and noise realizations").
 
-``ser_predicted`` needs the large-system analysis (``asymptotics.py``), which
-is out of scope for this build; it is reported as ``None``.
+``ser_predicted`` maps the large-system SINR (``asymptotics.asymptotic_sinr``,
+the message-passing MSE on the GPU quadratures) through ``ser_closed_form``
+as the reference does (montecarlo.py:188-194,217-218).
 """
 
 from __future__ import annotations
@@ -173,13 +174,22 @@ class SnrPointResult:
     ser: float
     ci_low: float
     ci_high: float
-    ser_predicted: float | None
+    ser_predicted: float
 
 
 @dataclass
 class SerResult:
     config: ExperimentConfig
     points: list = field(default_factory=list)
+
+
+def predicted_sinr(config, es_over_n0):
+    """Large-system SINR for the experiment's (equalizer, architecture)
+    (montecarlo.py:188-194)."""
+    from . import asymptotics
+
+    return asymptotics.asymptotic_sinr(config.equalizer, config.architecture, config.constellation, es_over_n0,
+                                       config.beta, weights=config.partition.weights)
 
 
 def count_errors(config, inp):
@@ -198,7 +208,8 @@ def run_experiment(config, inputs=None):
         inp = inputs[k] if inputs is not None else draw_inputs(config, k)
         errors = count_errors(config, inp)
         ci_low, ci_high = wilson_interval(errors / config.u, config.trials)
+        ser_pred = ser_closed_form(config.constellation, predicted_sinr(config, 10.0 ** (snr_db / 10.0)))
         result.points.append(SnrPointResult(
             snr_db=snr_db, trials=config.trials, n_symbols=n_symbols, errors=errors,
-            ser=errors / n_symbols, ci_low=ci_low, ci_high=ci_high, ser_predicted=None))
+            ser=errors / n_symbols, ci_low=ci_low, ci_high=ci_high, ser_predicted=ser_pred))
     return result

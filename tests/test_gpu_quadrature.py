@@ -56,3 +56,19 @@ def test_sweep_matches_oracle_and_limits():
     assert np.all(np.diff(mi) > -1e-12) and mi[0] < 0.01 and abs(mi[-1] - 4.0) < 1e-6  # saturates at log2 M
     for i in (0, 57, 133, 199):
         close(mi[i], O.mi_awgn(c.es / sinr[i], c.symbols, 12), rtol=1e-10)
+
+
+@pytest.mark.parametrize("tag,beta,c", [("small", 8 / 64, 2), ("crit8", 16 / 256, 8)])
+def test_message_passing_fixed_points_match_reference(tag, beta, c):
+    """LAMA's state-evolution fixed points (PD / centralized) and per-cluster
+    FD fixed points, iterated on the GPU quadrature, give the reference's
+    SINRs; the Monte Carlo driver's ser_predicted follows."""
+    q16 = dbp.make_constellation("qam16")
+    w = np.full(c, 1.0 / c)
+    for arch in ("pd", "fd", "centralized"):
+        got = [A.asymptotic_sinr("lama", arch, q16, 10.0 ** (x / 10.0), beta, weights=w) for x in G[f"sinr_{tag}_snr"]]
+        close(got, G[f"sinr_{tag}_lama_{arch}"], rtol=1e-9)
+    if tag == "small":
+        from paper_1808_04473_b200 import montecarlo as mc
+
+        close([mc.ser_closed_form(q16, x) for x in G["sinr_small_lama_fd"]], G["ser_pred_q16"], rtol=1e-12)
