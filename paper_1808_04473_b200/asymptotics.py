@@ -16,8 +16,9 @@ the Monte Carlo driver maps to ``ser_predicted`` (asymptotics.py:75-111,
 132-235, 291-316): ``solve_fixed_point``, ``sinr_pd_closed_form``,
 ``sinr_fd``, ``sinr_fd_zf_closed``, ``sinr_fd_lmmse_closed``,
 ``asymptotic_sinr`` -- scalar host iterations whose only heavy step, the
-message-passing MSE, is the GPU quadrature.  The rate searches
-(``sinr_for_rate``, ``min_antenna_ratio``) stay out of scope.
+message-passing MSE, is the GPU quadrature; and the rate searches
+``sinr_for_rate`` / ``min_antenna_ratio`` (asymptotics.py:265-376), the same
+bisections over those functions.
 """
 
 from __future__ import annotations
@@ -31,7 +32,7 @@ import math
 
 from . import _lib
 from .equalize import Equalizer
-from .errors import ConfigError, InvalidRegimeError, NonConvergenceError
+from .errors import ConfigError, InfeasibleError, InvalidRegimeError, NonConvergenceError
 from .model import Architecture
 
 DEFAULT_QUAD_ORDER = 32  # kernels.py:22
@@ -306,3 +307,67 @@ def asymptotic_sinr(kind, architecture, constellation, es_over_n0, beta, weights
         spec = MseSpec(Equalizer.LAMA, es=constellation.es, constellation=constellation, order=order)
         return solve_fixed_point(spec, constellation.es / es_over_n0, beta).sinr
     return sinr_pd_closed_form(kind, es_over_n0, beta)
+
+
+def sinr_for_rate(constellation, rate, tol_bits=1e-9, order=DEFAULT_QUAD_ORDER):
+    """asymptotics.py:265-288: the SINR at which the AWGN mutual information
+    of the constellation reaches ``rate`` bits (doubling, then bisection)."""
+    max_rate = constellation.bits_per_symbol
+    if not 0.0 < rate < max_rate:
+        raise ConfigError(f"target rate must lie in (0, {max_rate}), got {rate}")
+    hi = 1.0
+    for _ in range(80):
+        if awgn_mutual_information(constellation, hi, order) >= rate:
+            break
+        hi *= 2.0
+    else:
+        raise InfeasibleError(f"rate {rate} not reachable at finite SINR")
+    lo = 0.0
+    while True:
+        mid = 0.5 * (lo + hi)
+        mi = awgn_mutual_information(constellation, mid, order)
+        if abs(mi - rate) <= tol_bits or (hi - lo) <= 1e-12 * max(hi, 1.0):
+            return mid
+        if mi < rate:
+            lo = mid
+        else:
+            hi = mid
+
+
+def min_antenna_ratio(kind, architecture, constellation, target_rate, snr_loss_db, c=1, weights=None,
+                      beta_resolution=1e-4, order=None):
+    """asymptotics.py:319-376: smallest B/U at which the equalizer, at
+    ``snr_loss_db`` above the AWGN SNR for ``target_rate``, still reaches it
+    (bisection on beta; LAMA's feasible set is re-checked on a grid)."""
+    kind = Equalizer(kind)
+    architecture = Architecture(architecture)
+    if snr_loss_db < 0:
+        raise ConfigError("SNR loss must be nonnegative")
+    if weights is None:
+        weights = np.full(c, 1.0 / c)
+    gamma = sinr_for_rate(constellation, target_rate, order=order or DEFAULT_QUAD_ORDER)
+    g = gamma * 10.0 ** (snr_loss_db / 10.0)
+
+    def feasible(beta):
+        try:
+            return asymptotic_sinr(kind, architecture, constellation, g, beta, weights, order=order) >= gamma
+        except InvalidRegimeError:
+            return False
+
+    lo = 1e-6
+    if not feasible(lo):
+        raise InfeasibleError(f"no antenna ratio up to 1e6 achieves rate {target_rate} at {snr_loss_db} dB SNR loss")
+    if feasible(1.0):
+        return 1.0
+    hi = 1.0
+    while hi - lo > beta_resolution:
+        mid = 0.5 * (lo + hi)
+        if feasible(mid):
+            lo = mid
+        else:
+            hi = mid
+    if kind is Equalizer.LAMA and any(feasible(b) for b in np.linspace(hi, 1.0, 65)[1:]):
+        for b in np.arange(1.0, hi, -beta_resolution):  # disconnected feasible set: fine scan
+            if feasible(b):
+                return 1.0 / b
+    return 1.0 / lo

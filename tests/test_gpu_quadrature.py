@@ -72,3 +72,17 @@ def test_message_passing_fixed_points_match_reference(tag, beta, c):
         from paper_1808_04473_b200 import montecarlo as mc
 
         close([mc.ser_closed_form(q16, x) for x in G["sinr_small_lama_fd"]], G["ser_pred_q16"], rtol=1e-12)
+
+
+def test_rate_searches_match_reference():
+    """sinr_for_rate (bisection on the GPU mutual information) and
+    min_antenna_ratio (bisection on asymptotic_sinr, LAMA via GPU fixed
+    points) return the reference's values."""
+    q16 = dbp.make_constellation("qam16")
+    got = [A.sinr_for_rate(q16, r, order=16) for r in G["rate_targets"]]
+    close(got, G["sinr_for_rate_q16"], rtol=1e-9)
+    cases = [("lmmse", "pd", 1), ("zf", "fd", 4), ("mrc", "pd", 1), ("lmmse", "fd", 8), ("lama", "pd", 1)]
+    got = [A.min_antenna_ratio(k, a, q16, 2.0, 3.0, c=c, order=16) for k, a, c in cases]
+    close(got, G["mar_q16"], rtol=1e-9)
+    with pytest.raises(dbp.ConfigError):
+        A.sinr_for_rate(q16, 4.0)
