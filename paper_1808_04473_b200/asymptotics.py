@@ -200,6 +200,21 @@ def solve_fixed_point(spec, n0, beta, w=1.0, tol=1e-12, max_iter=100_000):
                               f"(kind={spec.kind}, beta={beta}, w={w})")
 
 
+def fixed_point_multiplicity(spec, n0, beta, w=1.0, rel_tol=1e-6):
+    """asymptotics.py:112-129: rerun the iteration from just above the noise
+    floor; a different limit than the largest fixed point means several
+    solutions.  Returns (multiple, largest, smallest)."""
+    largest = solve_fixed_point(spec, n0, beta, w=w).sigma2
+    sigma2 = n0 / w * (1.0 + 1e-9)
+    for _ in range(100_000):
+        nxt = (n0 + beta * psi_mse(spec, sigma2)) / w
+        done = abs(nxt - sigma2) <= 1e-12 * sigma2
+        sigma2 = nxt
+        if done:
+            break
+    return abs(largest - sigma2) > rel_tol * largest, largest, min(sigma2, largest)
+
+
 def _lmmse_cluster_sinr(g, beta, w):
     """Per-cluster L-MMSE SINR for an antenna fraction w (asymptotics.py:148-152):
     the positive root of s^2 + (1 - g (w - beta)) s - g w = 0."""

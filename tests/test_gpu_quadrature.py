@@ -86,3 +86,12 @@ def test_rate_searches_match_reference():
     close(got, G["mar_q16"], rtol=1e-9)
     with pytest.raises(dbp.ConfigError):
         A.sinr_for_rate(q16, 4.0)
+
+
+def test_fixed_point_multiplicity_matches_reference():
+    q16 = dbp.make_constellation("qam16")
+    spec = A.MseSpec("lama", es=q16.es, constellation=q16, order=32)
+    for (n0, beta), want, mult in zip(((0.05, 0.5), (0.02, 1.4), (0.2, 2.0)), G["fpm_q16"], G["fpm_q16_multiple"]):
+        m, hi, lo = A.fixed_point_multiplicity(spec, n0, beta)
+        assert m == bool(mult)
+        close([hi, lo], want, rtol=1e-8)
