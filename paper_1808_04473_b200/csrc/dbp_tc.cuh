@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     // assembler adds the partials.  Two issuing threads overlap one another's
     // wait / fence / commit latency.
     const int mw = warp - 1;
-    if (lane == 0) {
+    if (lane == 0 && !(p.ablate & 128)) {  // ablate 128: stream-only skeleton
       const uint32_t idesc = umma_idesc_tf32_mn(128, N);
       const uint32_t lbo = (uint32_t)L.lbo;
       const uint32_t ops = smem_u32(smem + L.ops);
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (h < pair && real[h]) wc.wait(&raw_full[gpos[h]], gph[h], 1);
-          if (pq >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
+          if (pq >= TC_NOP && !(p.ablate & 128)) wc.wait(&op_empty[b], bph ^ 1u, 1);
           const long long t_body = rec ? clock64() : 0;
           char* hi = smem + L.ops + 2 * b * L.opb;
           char* lo = hi + L.opb;
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           }
           if (rec) cnt[2] += clock64() - t_body;
           fence_proxy_async_smem();
-          mbar_arrive(&op_full[b]);
+          if (!(p.ablate & 128)) mbar_arrive(&op_full[b]);
           // an item's stage is free after its last chunk (multi-item stages:
           // after the group's last item)
           if (j == cpu - 1) {
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           sslot[h] = pos;
           wc.wait(&raw_full[pos], sp, 1);
         }
-        if (pq >= TC_NOP) wc.wait(&op_empty[b], bph ^ 1u, 1);
+        if (pq >= TC_NOP && !(p.ablate & 128)) wc.wait(&op_empty[b], bph ^ 1u, 1);
         const long long t_body = rec ? clock64() : 0;
         char* hi = smem + L.ops + 2 * b * L.opb;
         char* lo = hi + L.opb;
@@ -705,8 +705,8 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         }
         const long long t_fence = rec ? clock64() : 0;
         if (rec) cnt[2] += t_fence - t_body;
-        fence_proxy_async_smem();
-        mbar_arrive(&op_full[b]);
+        if (!(p.ablate & 256)) fence_proxy_async_smem();  // ablate 256: timing study only
+        if (!(p.ablate & 128)) mbar_arrive(&op_full[b]);
         if (rec) cnt[3] += clock64() - t_fence;
         // release a stage after the last chunk that reads it (host-computed
         // per item; a multi-item stage after its last item)
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
     const bool warp_rows = 32 * wq < MU;
     int ssl = 0;  // solver slot of unit v * pair (round robin, no divisions)
     uint32_t sph = 0;
-    for (int v = 0; v < n_pairs; ++v) {
+    for (int v = 0; v < ((p.ablate & 128) ? 0 : n_pairs); ++v) {
       const int a = v & 1;
       int slot[2];
       uint32_t sphase[2];
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       ++il;
     }
     uint32_t ph = 0;
-    for (int u = sv; u < U_tot; u += nsolv, ph ^= 1u) {
+    for (int u = sv; u < ((p.ablate & 128) ? 0 : U_tot); u += nsolv, ph ^= 1u) {
       const int64_t n = first + il;
       const bool item_end = (c == upi - 1);
       const float n0 = item_n0(p, n);  // global load issued before the wait

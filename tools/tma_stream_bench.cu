@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_1808_04473_b200/csrc/dbp_device.cuh"
+#ifndef CONSUMER_WARPS
+#define CONSUMER_WARPS 1  // warps that wait on every stage and release it (the kernel has 4 converters)
+#endif
 using namespace dbp;
 
 struct Cfg {
@@ -17,16 +20,19 @@ struct Cfg {
   int stages;       // ring depth (items)
   int lanes;        // issuing lanes
   int contiguous;   // items contiguous per CTA
+  int rows;         // > 0: tensor-core kernel pattern: one copy of the first (item_bytes - rows * rowb)
+  int rowb;         //      bytes, then `rows` copies of rowb bytes to 16-byte padded slots
+  const char* src2; // non-null: the row copies read a second array (H and Y as separate tensors)
 };
 
-__global__ void __launch_bounds__(128, 1) stream(Cfg c, long long* sink) {
+__global__ void __launch_bounds__(32 * (CONSUMER_WARPS + 1), 1) stream(Cfg c, long long* sink) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint64_t full[16], empty[16];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < c.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 32);
+      mbar_init(&empty[s], 32 * CONSUMER_WARPS);
     }
     fence_mbar_init();
   }
@@ -44,16 +50,26 @@ __global__ void __launch_bounds__(128, 1) stream(Cfg c, long long* sink) {
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)c.item_bytes);
       __syncwarp();
-      for (int q = lane; q < c.split; q += c.lanes)
-        if (lane < c.lanes)
-          bulk_g2s(smem + s * c.item_bytes + q * cb, c.src + n * c.item_bytes + q * cb, cb, &full[s], pol);
+      if (c.rows > 0) {
+        const int hb = c.item_bytes - c.rows * c.rowb;
+        char* dst = smem + s * (c.item_bytes + 16 * c.rows);
+        const char* src = c.src2 ? c.src + n * hb : c.src + n * c.item_bytes;
+        const char* ysrc = c.src2 ? c.src2 + n * (c.item_bytes - hb) : src + hb;
+        if (lane == 0) bulk_g2s(dst, src, hb, &full[s], pol);
+        for (int r = lane; r < c.rows; r += 32)
+          bulk_g2s(dst + hb + r * (c.rowb + 16), ysrc + r * c.rowb, c.rowb, &full[s], pol);
+      } else {
+        for (int q = lane; q < c.split; q += c.lanes)
+          if (lane < c.lanes)
+            bulk_g2s(smem + s * c.item_bytes + q * cb, c.src + n * c.item_bytes + q * cb, cb, &full[s], pol);
+      }
     }
-  } else if (warp == 1) {
+  } else if (warp <= CONSUMER_WARPS) {
     long long acc = 0;
     for (long long k = 0; k < my; ++k) {
       const int s = (int)(k % c.stages);
       mbar_wait(&full[s], (uint32_t)((k / c.stages) & 1));
-      acc += reinterpret_cast<const int*>(smem + s * c.item_bytes)[lane];
+      acc += reinterpret_cast<const int*>(smem + s * (c.item_bytes + 16 * c.rows))[lane];
       mbar_arrive(&empty[s]);
     }
     if (acc == 12345) sink[0] = acc;
@@ -73,27 +89,33 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  struct V { int item, split, stages, lanes, contig; };
+  struct V { int item, split, stages, lanes, contig, rows = 0, rowb = 0, sep = 0; };
   const V vs[] = {
       {61440, 2, 2, 2, 1}, {61440, 2, 3, 2, 1}, {30720, 2, 2, 2, 1}, {30720, 2, 3, 2, 1}, {30720, 2, 4, 2, 1},
       {30720, 2, 6, 2, 1}, {45056, 2, 2, 2, 1}, {45056, 2, 4, 2, 1}, {92160, 2, 2, 2, 1}, {15360, 2, 8, 2, 1},
       // cfg2 stage geometry: 2 items (H 2 x 16 KB) + 28 Y rows of 1 KB = 30 copies of ~2 KB
       {61440, 30, 2, 32, 1}, {61440, 60, 2, 32, 1}, {61440, 15, 2, 32, 1}, {30720, 15, 3, 32, 1},
+      // the cfg2 tensor-core producer: 2 items per stage = one 32 KB H copy + 28 Y rows of 1 KB
+      {61440, 1, 2, 32, 1, 28, 1024}, {61440, 1, 3, 32, 1, 28, 1024}, {61440, 1, 2, 32, 1, 14, 2048},
+      // ... with H and Y in separate arrays, as the detector's inputs are
+      {61440, 1, 2, 32, 1, 28, 1024, 1}, {61440, 1, 3, 32, 1, 28, 1024, 1},
   };
   for (const V& v : vs) {
-    Cfg c{src, total / v.item, v.item, v.split, v.stages, v.lanes, v.contig};
-    if ((long long)v.item * v.stages > 200 * 1024) continue;
-    for (int rep = 0; rep < 2; ++rep) stream<<<sms, 128, v.item * v.stages>>>(c, sink);
+    Cfg c{src, total / v.item, v.item, v.split, v.stages, v.lanes, v.contig, v.rows, v.rowb,
+          v.sep ? src + (total / v.item) * (long long)(v.item - v.rows * v.rowb) : nullptr};
+    const int sb = (v.item + 16 * v.rows) * v.stages;
+    if (sb > 200 * 1024) continue;
+    for (int rep = 0; rep < 2; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1), sb>>>(c, sink);
     cudaEventRecord(a);
     const int R = 5;
-    for (int rep = 0; rep < R; ++rep) stream<<<sms, 128, v.item * v.stages>>>(c, sink);
+    for (int rep = 0; rep < R; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1), sb>>>(c, sink);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
-    printf("item %6d B split %2d (copy %6d B) stages %2d lanes %2d %s: %7.1f GB/s  %s\n", v.item, v.split,
-           v.item / v.split, v.stages, v.lanes, v.contig ? "contig " : "strided", (double)total * R / (ms * 1e6),
-           cudaGetErrorString(e));
+    printf("item %6d B split %2d (copy %6d B) rows %2d x %4d B stages %2d lanes %2d %s: %7.1f GB/s  %s\n", v.item,
+           v.split, v.item / v.split, v.rows, v.rowb, v.stages, v.lanes, v.contig ? "contig " : "strided",
+           (double)total * R / (ms * 1e6), cudaGetErrorString(e));
   }
   return 0;
 }
