@@ -7,6 +7,12 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_1808_04473_b200/csrc/dbp_device.cuh"
+#ifndef EXTRA_WARPS
+#define EXTRA_WARPS 0  // idle warps parked at the final barrier (the kernel has 16 warps)
+#endif
+#ifndef EXTRA_SMEM
+#define EXTRA_SMEM 0  // extra dynamic shared memory (the kernel uses ~230 KB)
+#endif
 #ifndef CONSUMER_WARPS
 #define CONSUMER_WARPS 1  // warps that wait on every stage and release it (the kernel has 4 converters)
 #endif
@@ -25,7 +31,7 @@ struct Cfg {
   const char* src2; // non-null: the row copies read a second array (H and Y as separate tensors)
 };
 
-__global__ void __launch_bounds__(32 * (CONSUMER_WARPS + 1), 1) stream(Cfg c, long long* sink) {
+__global__ void __launch_bounds__(32 * (CONSUMER_WARPS + 1 + EXTRA_WARPS), 1) stream(Cfg c, long long* sink) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint64_t full[16], empty[16];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -74,6 +80,7 @@ __global__ void __launch_bounds__(32 * (CONSUMER_WARPS + 1), 1) stream(Cfg c, lo
     }
     if (acc == 12345) sink[0] = acc;
   }
+  __syncthreads();
 }
 
 int main() {
@@ -85,7 +92,7 @@ int main() {
   cudaMemset(src, 1, total);
   long long* sink;
   cudaMalloc(&sink, 8);
-  cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -104,11 +111,11 @@ int main() {
     Cfg c{src, total / v.item, v.item, v.split, v.stages, v.lanes, v.contig, v.rows, v.rowb,
           v.sep ? src + (total / v.item) * (long long)(v.item - v.rows * v.rowb) : nullptr};
     const int sb = (v.item + 16 * v.rows) * v.stages;
-    if (sb > 200 * 1024) continue;
-    for (int rep = 0; rep < 2; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1), sb>>>(c, sink);
+    if (sb + EXTRA_SMEM > 226 * 1024) continue;
+    for (int rep = 0; rep < 2; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1 + EXTRA_WARPS), sb + EXTRA_SMEM>>>(c, sink);
     cudaEventRecord(a);
     const int R = 5;
-    for (int rep = 0; rep < R; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1), sb>>>(c, sink);
+    for (int rep = 0; rep < R; ++rep) stream<<<sms, 32 * (CONSUMER_WARPS + 1 + EXTRA_WARPS), sb + EXTRA_SMEM>>>(c, sink);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0;
