@@ -402,9 +402,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
       for (int k = 0; k < spi; ++k, ++seq) {
         const int r0 = st_row0[k], R = st_rows[k];
         const uint32_t hb = (uint32_t)cnt * R * p.us * 8, yb = (uint32_t)cnt * T * R * 8;  // bytes landing
+        const bool no_y = (p.ablate & 512) != 0;  // timing study only: H copies alone
         if (lane == 0) {
           if (seq >= NS) wc.wait(&raw_empty[s], ph ^ 1u, 2);
-          mbar_arrive_expect_tx(&raw_full[s], hb + yb);
+          mbar_arrive_expect_tx(&raw_full[s], no_y ? hb : hb + yb);
         }
         __syncwarp();
         char* dst = smem + L.stg + s * L.sbytes;
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         } else if (lane == 0) {
           bulk_g2s(dst, p.H + ((size_t)n0 * p.B + r0) * p.us, hb, &raw_full[s], policy);
         }
-        for (int r = lane; r < cnt * T; r += 32)
+        for (int r = lane; r < (no_y ? 0 : cnt * T); r += 32)
           bulk_g2s(dst + p.stage_hbytes + r * p.stage_ystride, p.Y + ((size_t)n0 * T + r) * p.B + r0, R * 8,
                    &raw_full[s], policy);
         if (++s == NS) {
