@@ -566,6 +566,18 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
           }
         }
       }
+      if (p.ablate & 1024) {  // timing study only: one wait + release per stage, no chunk loop
+        if (spi == 1) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (h < pair && real[h]) wc.wait(&raw_full[gpos[h]], gph[h], 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (h < pair && real[h] && cl[h] == upi - 1 && (sl[h] == ips - 1 || il[h] == my_items - 1))
+              mbar_arrive(&raw_empty[gpos[h]]);
+        }
+        continue;
+      }
       for (int j = 0; j < cpu; ++j) {
         const int pq = v * cpu + j;
         if ((pq % TC_CONV_SETS) != cset) continue;
@@ -574,9 +586,14 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
         if (p.tc_simple && !(p.ablate & 4)) {
           // simple geometry: every address is arithmetic (no table lookups:
           // a lone warp pays ~30 cycles per dependent shared-memory load)
+          // one stage holds every chunk of the pair's items (spi == 1): wait
+          // for it once, at the first chunk (a completed-phase wait per chunk
+          // costs the converter hundreds of cycles: stream-only study)
+          if (j == 0) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (h < pair && real[h]) wc.wait(&raw_full[gpos[h]], gph[h], 1);
+            for (int h = 0; h < 2; ++h)
+              if (h < pair && real[h]) wc.wait(&raw_full[gpos[h]], gph[h], 1);
+          }
           if (pq >= TC_NOP && !(p.ablate & 128)) wc.wait(&op_empty[b], bph ^ 1u, 1);
           const long long t_body = rec ? clock64() : 0;
           char* hi = smem + L.ops + 2 * b * L.opb;
@@ -613,7 +630,7 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
             }
           }
           if (rec) cnt[2] += clock64() - t_body;
-          fence_proxy_async_smem();
+          if (!(p.ablate & 256)) fence_proxy_async_smem();  // ablate 256: timing study only
           if (!(p.ablate & 128)) mbar_arrive(&op_full[b]);
           // an item's stage is free after its last chunk (multi-item stages:
           // after the group's last item)
