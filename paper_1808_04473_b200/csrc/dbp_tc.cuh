@@ -36,6 +36,12 @@
 // Everything is pipelined through mbarriers: loads, conversions and MMAs of
 // later units overlap the solves of earlier ones, and several units are
 // solved concurrently.
+//
+// DBP_ABLATE (timing studies only; results are wrong when set): 1 no solver
+// work, 2 no MMAs, 4 no conversion, 32 no TMEM read-back, 64 LAMA team
+// schedule, 128 no operand ring / MMA / assembly / solve (stream + convert),
+// 256 no proxy fence, 512 H copies only, 1024 one stage wait + release per
+// pair (with 128: stream only).  tools/gpu_ablate.sh, tools/gpu_skel.sh.
 #pragma once
 #include "dbp_simt.cuh"
 
