@@ -56,3 +56,23 @@ def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
     assert np.mean(res.decisions.cpu().numpy() != ref.decisions) < 1e-3
     if arch == "fd":
         assert np.max(np.abs(res.nu.cpu().numpy() - ref.nu)) < 2e-6
+
+
+@pytest.mark.parametrize("arch", ["pd", "fd"])
+def test_cluster_group_u64_equals_fused(golden, nccl1, arch):
+    """U = 64 (cfg5a): the multi-GPU PD path's per-rank statistics run on the
+    wide tensor-core layout, FD's per-cluster partial sums on the SIMT kernel;
+    both equal the fused single-GPU detector."""
+    from paper_1808_04473_b200.distributed import ClusterGroup
+
+    g = golden("cfg5a")
+    const = dbp.make_constellation("qam64")
+    b, c, u = int(g["B"]), int(g["C"]), int(g["U"])
+    H = torch.from_numpy(g["H"]).cuda()
+    Y = torch.from_numpy(g["Y"]).cuda()
+    n0 = torch.tensor(g["n0"], dtype=torch.float32, device="cuda")
+    grp = ClusterGroup(arch, "lmmse", [b // c] * c, u, Y.shape[1], const)
+    res = grp.run(H, Y, n0)
+    ref = dbp.detect(arch, "lmmse", g["H"], g["Y"], g["n0"], [b // c] * c, const)
+    assert normwise_rel(res.xhat.cpu().numpy(), ref.xhat) < 1e-5
+    assert np.mean(res.decisions.cpu().numpy() != ref.decisions) < 1e-3
