@@ -85,7 +85,7 @@ def _quad(kind, xs, values, order):
 
 def _check_positive(v, what):
     if np.any(np.asarray(v) <= 0):
-        raise ConfigError(f"{what} must be > 0")
+        raise ConfigError(f"{what} must be > 0, got {v}")
 
 
 def lama_mse_pam(sigma2, levels, order=DEFAULT_PAM_ORDER):
@@ -125,7 +125,7 @@ class MseSpec:
 
 def psi_mse(spec, sigma2):
     """asymptotics.py:47-72: MSE of the equalizer's decoupled denoiser."""
-    _check_positive(sigma2, "MSE function requires sigma2")
+    _check_positive(sigma2, "the MSE function's sigma2")
     s = np.asarray(sigma2, dtype=np.float64)
     kind = spec.kind
     if kind is Equalizer.MRC:
