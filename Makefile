@@ -1,18 +1,26 @@
 # Builds the in-tree sm_100a shared library (travels to the GPU box with the repo snapshot).
+# One object per translation unit so `make -j` compiles the kernel families in parallel.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
-SRC := paper_1808_04473_b200/csrc/dbp_kernels.cu
-HDR := $(wildcard paper_1808_04473_b200/csrc/*.cuh) include/dbp_b200.h
+CSRC := paper_1808_04473_b200/csrc
+SRCS := $(CSRC)/dbp_kernels.cu $(CSRC)/dbp_launch_tc2.cu $(CSRC)/dbp_launch_tc.cu $(CSRC)/dbp_launch_simt.cu
+OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+HDR := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dbp_host.h include/dbp_b200.h
 LIB := paper_1808_04473_b200/libdbp_b200.so
 
 all: $(LIB)
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+build/%.o: $(CSRC)/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) $(EXTRA) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	@cat build/*.ptxas.log > build_ptxas.log
 	@grep -E "registers|spill|Compiling entry" build_ptxas.log | sed 's/ptxas info    : //' > paper_1808_04473_b200/ptxas_summary.txt || true
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -rf build $(LIB) build_ptxas.log
 
 .PHONY: all clean

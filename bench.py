@@ -434,8 +434,10 @@ def single_gpu(args, wl, name):
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "kernel": ("dbp::tc_kernel<64, stats> (tensor cores, wide layout) + dbp::stats_kernel<64> "
                                 "(solves), 2 launches/step" if two_pass else
-                                f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (tensor cores, 1 launch/step)"
-                                if kernel_id == 2 else
+                                f"dbp::tc2_kernel<{wl['arch'].upper()}-{wl['kind']}> (split-bf16 tensor cores, "
+                                f"1 launch/step)" if kernel_id == 3 else
+                                f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (3xTF32 tensor cores, "
+                                f"1 launch/step)" if kernel_id == 2 else
                                 f"dbp::stream_kernel<{up}> (FP32 SIMT, 1 launch/step)")},
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -76,10 +76,27 @@ extern "C" {
 int dbp_abi_version(void);
 const char* dbp_last_error(void);
 /* Which fused kernel the calling thread's last dbp_equalize / dbp_gram_mrc
- * launched: 2 = tensor-core streaming kernel (U <= 32, uniform clusters),
- * 1 = FP32-SIMT streaming kernel (U = 64 or ragged clusters), 0 = none.
- * Introspection only (tests and benchmarks); no reference counterpart. */
+ * launched (DBP_KERNEL_*; 0 = none).  Introspection only (tests and
+ * benchmarks); no reference counterpart. */
+#define DBP_KERNEL_AUTO 0
+#define DBP_KERNEL_SIMT 1     /* FP32-SIMT streaming kernel (U = 64, ragged clusters, LAMA) */
+#define DBP_KERNEL_TC_TF32 2  /* 3xTF32 tensor-core streaming kernel (U <= 32; U = 64 statistics) */
+#define DBP_KERNEL_TC_BF16 3  /* split-bf16 tensor-core streaming kernel (U <= 16 linear / statistics) */
 int dbp_last_kernel(void);
+
+/* Process-wide options for tests and A/B studies; all default to 0
+ * (automatic).  Returns the previous value (or DBP_E_ARG).  Nothing in the
+ * library reads the environment. */
+#define DBP_OPT_KERNEL 0      /* force a DBP_KERNEL_* (it must cover the geometry) */
+#define DBP_OPT_TC_SMAX_KB 1  /* tf32 kernel: max stage size (KB) */
+#define DBP_OPT_TC_NS 2       /* tf32 kernel: stage ring depth */
+#define DBP_OPT_TC_PAIR 3     /* tf32 kernel: units per operand tile (1, 2) */
+#define DBP_OPT_TC_NSOLV 4    /* tf32 kernel: solver warps */
+#define DBP_OPT_SIMT_NS 5     /* SIMT kernel: stage ring depth */
+#define DBP_OPT_NO_WIDE 6     /* U = 64: SIMT statistics instead of the tensor cores */
+#define DBP_OPT_T2_NSPLIT 7   /* split-bf16 kernel: bf16 parts per operand (2, 3) */
+#define DBP_OPT_COUNT 8
+int dbp_set_option(int key, int value);
 int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_bytes);
 
 /* Per-cluster Gram + matched filter.  Replaces local_preprocess

@@ -22,6 +22,11 @@ ABI_VERSION = 1
 ST_OK, ST_SINGULAR, ST_NEGVAR, ST_DIVERGED, ST_BADVAR = 0, 1, 2, 3, 4
 KIND = {"mrc": 0, "zf": 1, "lmmse": 2, "lama": 3}
 ARCH_PD, ARCH_FD, ARCH_FD_PARTIAL = 1, 2, 3
+# fused kernels (dbp_last_kernel / DBP_OPT_KERNEL)
+KERNEL_AUTO, KERNEL_SIMT, KERNEL_TC_TF32, KERNEL_TC_BF16 = 0, 1, 2, 3
+# dbp_set_option keys
+OPTIONS = {"kernel": 0, "tc_smax_kb": 1, "tc_ns": 2, "tc_pair": 3, "tc_nsolv": 4, "simt_ns": 5,
+           "no_wide": 6, "t2_nsplit": 7}
 
 _vp, _fp, _i32p, _u8p = C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p
 _i64, _i, _f = C.c_int64, C.c_int, C.c_float
@@ -31,6 +36,7 @@ SIGNATURES = {
     "dbp_abi_version": [],
     "dbp_last_error": [],
     "dbp_last_kernel": [],
+    "dbp_set_option": [_i, _i],
     "dbp_device_query": [_vp, _vp, _vp, _vp],
     "dbp_gram_mrc": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp],
     "dbp_equalize_stats": [_vp, _i64, _i, _i, _i, _f, _vp, _i64, _f, _i, _f, _f, _i, _f,
@@ -118,3 +124,27 @@ def host_i32(values):
 
     arr = np.ascontiguousarray(np.asarray(values, dtype=np.int32).reshape(-1))
     return arr, arr.ctypes.data_as(C.c_void_p)
+
+
+class options:
+    """Context manager over dbp_set_option (kernel selection and staging
+    overrides for tests and A/B studies), e.g.
+    ``with _lib.options(kernel=KERNEL_SIMT): ...``.  Restores the previous
+    values on exit."""
+
+    def __init__(self, **kw):
+        unknown = set(kw) - set(OPTIONS)
+        if unknown:
+            raise ValueError(f"unknown options {sorted(unknown)}")
+        self.kw = kw
+        self.prev = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.prev[k] = lib().dbp_set_option(OPTIONS[k], int(v))
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.prev.items():
+            lib().dbp_set_option(OPTIONS[k], v)
+        return False

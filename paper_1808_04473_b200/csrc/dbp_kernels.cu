@@ -14,14 +14,17 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/dbp_b200.h"
 #include "dbp_device.cuh"
 #include "dbp_epilogue.cuh"
-#include "dbp_simt.cuh"
-#include "dbp_tc.cuh"
+#include "dbp_host.h"
 #include "dbp_synth.cuh"
 
 namespace dbp {
@@ -322,9 +325,12 @@ __global__ void unbias_kernel(const float2* __restrict__ z, const float* __restr
     if (!(c > 0.f)) atomicCAS(status + item, 0, ST_SINGULAR);
     z_out[e] = c_scale(z[e], 1.f / c);
     if (t == 0) {
-      const float d = 1.f - c;
-      const float v = (s2[item * u + i] - d * d * es) / (c * c);
-      if (v < -1e-9f) atomicCAS(status + item, 0, ST_NEGVAR);
+      const float d = 1.f - c, a = s2[item * u + i], b = d * d * es;
+      const float v = (a - b) / (c * c);
+      // _VAR_TOL = 1e-9 (equalize.py:24) plus the fp32 rounding level of the
+      // difference, so rounding-level negatives clamp instead of raising
+      const float tol = 1e-9f + 4.f * FLT_EPSILON * (fabsf(a) + b) / (c * c);
+      if (v < -tol) atomicCAS(status + item, 0, ST_NEGVAR);
       s2_out[item * u + i] = fmaxf(v, 0.f);
     }
   }
@@ -373,20 +379,28 @@ __global__ void fuse_estimates_kernel(const float2* __restrict__ z, const float*
 using namespace dbp;
 
 static thread_local std::string g_err;
-static thread_local int g_last_kernel = 0;  // dbp_last_kernel()
+thread_local int g_last_kernel = 0;  // dbp_last_kernel()
 
-static int fail(int code, const std::string& msg) {
+// Process-wide kernel-selection / staging options (dbp_set_option): explicit
+// calls, never the environment, so a stray variable cannot change what the
+// library computes.  0 = automatic everywhere.
+static std::atomic<int> g_opt[DBP_OPT_COUNT];
+
+namespace dbp {
+int opt(int key) { return g_opt[key].load(std::memory_order_relaxed); }
+
+int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
 
-static int cuda_check(const char* where) {
+int cuda_check(const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DBP_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
   return DBP_OK;
 }
 
-static int sm_count() {
+int sm_count() {
   static int cached = -1;
   if (cached < 0) {
     int dev = 0;
@@ -396,6 +410,49 @@ static int sm_count() {
   }
   return cached;
 }
+
+// Per-(device, stream) device scratch (FD fold records, U = 64 statistics),
+// grown on demand.  Launches on one stream are ordered, so they may share it;
+// other streams (and other devices) get their own.  Growth is stream-ordered
+// (cudaFreeAsync of the old buffer, cudaMallocAsync of the new one on the same
+// stream): no host synchronisation inside a launch, capturable in a CUDA
+// graph.  The table is guarded by a mutex (calls are reentrant).
+void* stream_scratch(cudaStream_t st, size_t need) {
+  struct Entry {
+    int dev;
+    cudaStream_t st;
+    void* ptr;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static Entry tab[64];
+  static int used = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  Entry* e = nullptr;
+  for (int i = 0; i < used; ++i)
+    if (tab[i].st == st && tab[i].dev == dev) e = &tab[i];
+  if (!e) {
+    if (used == 64) return nullptr;
+    e = &tab[used++];
+    *e = Entry{dev, st, nullptr, 0};
+  }
+  if (need > e->bytes) {
+    if (e->ptr) cudaFreeAsync(e->ptr, st);  // freed after the work already queued on st
+    e->ptr = nullptr;
+    e->bytes = 0;
+    need = std::max(need, (size_t)1 << 20);
+    if (cudaMallocAsync(&e->ptr, need, st) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    e->bytes = need;
+  }
+  return e->ptr;
+}
+
+}  // namespace dbp
 
 static int up_for(int u) { return u <= 8 ? 8 : u <= 16 ? 16 : u <= 32 ? 32 : u <= 64 ? 64 : -1; }
 
@@ -419,286 +476,32 @@ static int fill_const(ConstParams& cp, const float* levels, int L, const float* 
   return DBP_OK;
 }
 
-template <int UP, int NT>
-static int launch_stream(EqParams& p, cudaStream_t st) {
-  const bool lama = p.kind == EQ_LAMA;
-  const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  const int TB = p.TP / 4;
-  constexpr int UB = UP / 4;
-  const int ntiles = UB * (UB + 1) / 2 + UB * TB;
-  const int S = NT / ntiles;
-  if (S < 1) return fail(DBP_E_UNSUPPORTED, "too many output tiles for the CTA (u, T too large)");
-  const int red_f2 = S > 1 ? (S - 1) * ntiles * 16 : 0;
-  auto kern = p.arch == ARCH_STATS ? stream_kernel<UP, NT, 0>
-              : p.kind == EQ_LAMA   ? stream_kernel<UP, NT, 2>
-                                    : stream_kernel<UP, NT, -1>;
-  // ring depth: the deepest ring (<= p.NS, >= 2) that still lets a second CTA
-  // share the SM, so one CTA's Gram overlaps the other's epilogue (U = 64:
-  // 3 stages = one CTA per SM; 2 stages = two, cfg5 57 -> 46 ms)
-  int per_sm = 0, ns = p.NS;
-  if (const char* e = getenv("DBP_SIMT_NS")) ns = std::max(2, atoi(e));  // tuning studies
-  SimtLayout L = make_simt_layout(UP, p.TP, p.stage_f2 * 8, ns, p.C, red_f2, lama, fd);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
-    return fail(DBP_E_CUDA, "shared memory request too large");
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, L.total);
-  for (int k = ns - 1; k >= 2 && per_sm < 2 && !getenv("DBP_SIMT_NS"); --k) {
-    const SimtLayout L2 = make_simt_layout(UP, p.TP, p.stage_f2 * 8, k, p.C, red_f2, lama, fd);
-    int per2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, kern, NT, L2.total);
-    if (per2 > per_sm) {
-      ns = k;
-      L = L2;
-      per_sm = per2;
-    }
-  }
-  p.NS = ns;
-  if (per_sm < 1) return fail(DBP_E_UNSUPPORTED, "kernel does not fit on an SM");
-  const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count() * per_sm);
-  kern<<<(unsigned)grid, NT, L.total, st>>>(p);
-  return cuda_check("stream_kernel");
-}
-
-// Per-stream device scratch (FD fold records), grown on demand.  Launches on
-// one stream are ordered, so they may share it; other streams get their own.
-static void* stream_scratch(cudaStream_t st, size_t need) {
-  struct Entry {
-    cudaStream_t st;
-    void* ptr;
-    size_t bytes;
-  };
-  static Entry tab[16];
-  static int used = 0;
-  Entry* e = nullptr;
-  for (int i = 0; i < used; ++i)
-    if (tab[i].st == st) e = &tab[i];
-  if (!e) {
-    if (used == 16) return nullptr;
-    e = &tab[used++];
-    *e = Entry{st, nullptr, 0};
-  }
-  if (need > e->bytes) {
-    if (e->ptr) {
-      cudaStreamSynchronize(st);  // the previous buffer may still be in use on this stream
-      cudaFree(e->ptr);
-    }
-    e->ptr = nullptr;
-    e->bytes = 0;
-    if (cudaMalloc(&e->ptr, need) != cudaSuccess) return nullptr;
-    e->bytes = need;
-  }
-  return e->ptr;
-}
-
-template <int UP>
-static int launch_tc(EqParams& p, cudaStream_t st) {
-  const bool lama = p.kind == EQ_LAMA;
-  const bool fd = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  // U = 64 ("wide": A = the 128 H features, B = [H | Y], N = 160) computes
-  // statistics only; its solves run in stats_kernel (dispatch_stream)
-  constexpr bool WIDE = UP > 32;
-  if (WIDE && p.arch != ARCH_STATS) return 1;
-  if (!WIDE && 2 * UP + 32 > 128) return fail(DBP_E_UNSUPPORTED, "2U + 32 > 128 rows on the tensor-core path");
-  int dev = 0, smem_max = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // two units per operand tile / MMA when both fit in M = 128 rows and every
-  // unit has the same chunk structure (uniform clusters for per-cluster units)
-  const bool per_cluster = fd || (p.arch == ARCH_STATS && !p.sum_clusters);
-  bool uniform = true;
-  const int upi = per_cluster ? p.C : 1;
-  if (p.nchunks % upi) uniform = false;
-  const int cpu = uniform ? p.nchunks / upi : 0;
-  for (int c = 1; uniform && c < upi; ++c)
-    for (int j = 0; j < cpu; ++j)
-      if (p.chunks[c * cpu + j].nrows != p.chunks[j].nrows || p.chunks[c * cpu + j].cluster != c) uniform = false;
-  if (!uniform) return 1;  // ragged clusters: SIMT kernel
-  // pair two units per tile when M allows; per-cluster units pair within an
-  // item (even cluster count), items pair within a stage
-  p.pair = (tc_yrow0(UP, 2) + 2 * 32 <= 128) ? 2 : 1;
-  if (upi > 1 && (upi & 1)) p.pair = 1;
-  if (const char* e = getenv("DBP_TC_PAIR")) p.pair = std::max(1, std::min(2, atoi(e)));
-  if (WIDE) p.pair = 1;
-  // staging plan: whole items (several per stage when small) or row blocks
-  const int hrow = p.us * 8, yrow = p.T * 8;  // bytes per antenna row of H / Y
-  const int item_bytes = p.B * (hrow + yrow);
-  int smax = 64 * 1024;
-  if (const char* e = getenv("DBP_TC_SMAX")) smax = atoi(e) * 1024;
-  int nsolv = TC_MAX_SOLV;
-  for (int attempt = 0;; ++attempt) {  // shrink the stages until the layout fits
-  // (paired items may sit in different stages: the converter waits for both,
-  // and the ring keeps at least 2 stages, all filled in order)
-  if (item_bytes <= smax) {
-    p.spi = 1;
-    p.ips = std::max(1, smax / item_bytes);
-    p.st_row0[0] = 0;
-    p.st_rows[0] = p.B;
-  } else {
-    // row blocks at chunk boundaries (cluster-pair boundaries when units pair
-    // inside an item), each at most smax bytes
-    p.ips = 1;
-    p.spi = 0;
-    const int unit_step = (p.pair == 2 && upi > 1) ? 2 : 1;
-    int r0 = 0, rows = 0;
-    for (int j = 0; j < p.nchunks; ++j) {
-      const ChunkDesc& cd = p.chunks[j];
-      const bool boundary = (cd.row0 == p.chunks[(cd.cluster / unit_step) * unit_step * cpu].row0) || !per_cluster;
-      if (rows > 0 && boundary && (rows + cd.nrows) * (hrow + yrow) + 16 * p.T > smax) {
-        if (p.spi == MAX_SPI) return 1;
-        p.st_row0[p.spi] = r0;
-        p.st_rows[p.spi++] = rows;
-        r0 = cd.row0;
-        rows = 0;
-      }
-      rows += cd.nrows;
-    }
-    if (p.spi == MAX_SPI) return 1;
-    p.st_row0[p.spi] = r0;
-    p.st_rows[p.spi++] = rows;
-  }
-  int rmax = 0;
-  for (int k = 0; k < p.spi; ++k) rmax = std::max(rmax, p.st_rows[k]);
-  // Y symbol rows are staged with a 16-byte pad (row stride = 65 16-byte
-  // chunks for 128 antennas) so that the converter's transposing loads of
-  // symbols 2tp, 2tp+1 spread over all banks
-  p.stage_hbytes = p.ips * rmax * hrow;
-  p.stage_ystride = rmax * 8 + 16;
-  p.stage_bytes = p.stage_hbytes + p.ips * p.T * p.stage_ystride;
-  // chunk -> stage, and the last chunk of the item's visit order touching
-  // each stage (units of an item in order; paired clusters interleave)
-  for (int j = 0; j < p.nchunks; ++j) {
-    int k = 0;
-    while (k + 1 < p.spi && p.chunks[j].row0 >= p.st_row0[k + 1]) ++k;
-    p.chunks[j].flags = (p.chunks[j].flags & 0xff) | (k << CH_STAGE_SHIFT);
-  }
-  {
-    int last[MAX_SPI];
-    for (int k = 0; k < MAX_SPI; ++k) last[k] = -1;
-    const int ps = (p.pair == 2 && upi > 1) ? 2 : 1;  // units of an item sharing a tile
-    for (int c0 = 0; c0 < upi; c0 += ps)
-      for (int j = 0; j < cpu; ++j)
-        for (int h = 0; h < ps; ++h) {
-          const int idx = (c0 + h) * cpu + j;
-          last[(p.chunks[idx].flags >> CH_STAGE_SHIFT) & 0xff] = idx;
-        }
-    for (int k = 0; k < p.spi; ++k)
-      if (last[k] >= 0) p.chunks[last[k]].flags |= CH_STAGE_REL;
-  }
-  // simple geometry: the converter derives every address arithmetically
-  // (chunk j of cluster c starts at row c * B/upi + 32 j) instead of through
-  // the chunk table
-  p.tc_bc = p.B / upi;
-  p.tc_simple = (p.spi == 1) && (p.B % upi == 0);
-  for (int c = 0; p.tc_simple && c < upi; ++c)
-    for (int j = 0; j < cpu; ++j) {
-      const ChunkDesc& cd = p.chunks[c * cpu + j];
-      if (cd.nrows != 32 || cd.row0 != c * p.tc_bc + 32 * j) p.tc_simple = 0;
-    }
-  auto fits = [&](int ns, int nsv) {
-    return make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, ns, p.C, lama, fd, nsv).total <= smem_max;
-  };
-  // ring depth: ~96 KB of stages when they fit (>= 2), then solver warps
-  p.NS = std::max(2, std::min(8, (96 * 1024 + p.stage_bytes - 1) / p.stage_bytes));
-  nsolv = TC_MAX_SOLV;
-  // tuning overrides (timing studies only)
-  if (const char* e = getenv("DBP_TC_NS")) p.NS = atoi(e);
-  if (const char* e = getenv("DBP_TC_NSOLV")) nsolv = std::max(2, std::min(TC_MAX_SOLV, atoi(e)));
-  while (nsolv > 4 && !fits(p.NS, nsolv)) --nsolv;
-  while (p.NS > 2 && !fits(p.NS, nsolv)) --p.NS;
-  while (nsolv > (WIDE ? 1 : 2) && !fits(p.NS, nsolv)) --nsolv;  // wide: one statistics writer suffices
-  if (fits(p.NS, nsolv)) break;
-  if (attempt == 6 || smax < 8 * 1024) return 1;  // does not fit: caller falls back to the SIMT kernel
-  smax = smax * 3 / 4;
-  }
-  const TcLayout L = make_tc_layout(UP, p.TP, p.stage_bytes, p.KC, p.NS, p.C, lama, fd, nsolv);
-  if (fd) {  // per-(item, cluster) fold records: L2-resident scratch, one per stream, grown on demand
-    const size_t need = (size_t)p.n_items * p.C * fd_record_floats(p.u, p.T, lama ? p.T : p.u) * sizeof(float);
-    p.fd_scratch = static_cast<float*>(stream_scratch(st, need));
-    if (!p.fd_scratch) return fail(DBP_E_CUDA, "FD scratch allocation failed");
-  }
-  const bool fdm = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
-  void (*kern)(EqParams, int) = tc_kernel<UP, TC_STATS>;
-  if constexpr (!WIDE)
-    kern = (p.arch == ARCH_STATS) ? tc_kernel<UP, TC_STATS>
-           : fdm ? (lama ? tc_kernel<UP, TC_FD_LAMA> : tc_kernel<UP, TC_FD_LIN>)
-                 : (lama ? tc_kernel<UP, TC_PD_LAMA> : tc_kernel<UP, TC_PD_LIN>);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
-    return fail(DBP_E_CUDA, "shared memory request too large");
-  const int threads = 32 * (TC_FIRST_SOLVER + nsolv);
-  const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count());
-  static float* dtile = nullptr;
-  if (getenv("DBP_TC_DUMP")) {
-    if (!dtile) cudaMalloc(&dtile, 128 * 1024);
-    p.dbg_tile = dtile;
-  }
-  static long long* dbg = nullptr;
-  const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
-  if (debug) {
-    if (!dbg) cudaMalloc(&dbg, 128 * sizeof(long long));
-    cudaMemsetAsync(dbg, 0, 128 * sizeof(long long), st);
-    p.dbg = dbg;
-  }
-  kern<<<(unsigned)grid, threads, L.total, st>>>(p, nsolv);
-  if (p.dbg_tile) {
-    static float ht[32768];
-    cudaMemcpy(ht, dtile, L.opb, cudaMemcpyDeviceToHost);
-    FILE* f = fopen("gpurun_out/tile_dump.bin", "wb");
-    if (f) {
-      fwrite(ht, 1, L.opb, f);
-      fclose(f);
-    }
-  }
-  if (debug) {
-    long long h[128];
-    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[dbp tc debug] NS=%d stage=%d B ips=%d spi=%d pair=%d nsolv=%d (cycles summed over CTAs)\n",
-            p.NS, p.stage_bytes, p.ips, p.spi, p.pair, nsolv);
-    for (int w = 0; w < threads / 32; ++w) {
-      const char* name = w == 0 ? "producer" : w < TC_FIRST_CONV ? "mma" : w < TC_FIRST_ASM ? "converter"
-                         : w < TC_FIRST_SOLVER ? "assembler" : "solver";
-      fprintf(stderr, "  w%-2d %-9s total %.3e  c1 %.3e  c2 %.3e  c3 %.3e\n", w, name, (double)h[w * 4],
-              (double)h[w * 4 + 1], (double)h[w * 4 + 2], (double)h[w * 4 + 3]);
-    }
-  }
-  return cuda_check("tc_kernel");
-}
-
-template <int UP, int NT>
-static int launch_stats(EqParams& p, cudaStream_t st) {
-  const bool lama = p.kind == EQ_LAMA;
-  const WorkLayout L = make_work_layout(0, UP, p.TP, 1, lama, false);
-  auto kern = stats_kernel<UP, NT>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
-    return fail(DBP_E_CUDA, "shared memory request too large");
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, L.total);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t grid = std::min<int64_t>(p.n_items, (int64_t)sm_count() * per_sm);
-  kern<<<(unsigned)grid, NT, L.total, st>>>(p);
-  return cuda_check("stats_kernel");
-}
-
 // U <= 32 -> tensor-core kernel; U = 64 -> SIMT kernel (2(U+T) > 128).
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
 static int dispatch_stats(EqParams& p, cudaStream_t st);
 
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
   p.g_hermitian = 1;  // the streaming kernels build G themselves (full Hermitian matrix)
-  const bool force_simt = getenv("DBP_FORCE_SIMT") && getenv("DBP_FORCE_SIMT")[0] == '1';
+  const int pol = opt(DBP_OPT_KERNEL);
+  const bool force_simt = pol == DBP_KERNEL_SIMT;
   const int up = up_for(p.u);
-  const bool force_tc = getenv("DBP_FORCE_TC") && getenv("DBP_FORCE_TC")[0] == '1';
-  // the tensor-core kernel solves one unit per warp: LAMA (10 iterations over
-  // T x U state) and FD-MRC (trivial solves, fold-bound) run faster on the
-  // CTA-cooperative epilogue of the SIMT kernel (measured, tools/gpu_simt_vs_tc.sh)
+  // U <= 16 linear / statistics: the split-bf16 tensor-core kernel
+  if ((pol == DBP_KERNEL_AUTO || pol == DBP_KERNEL_TC_BF16) && up <= 16) {
+    const int rc = launch_tc2(p, st);
+    if (rc == 0) g_last_kernel = DBP_KERNEL_TC_BF16;
+    if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = not covered
+    if (pol == DBP_KERNEL_TC_BF16) return fail(DBP_E_UNSUPPORTED, "geometry not covered by the split-bf16 kernel");
+  }
+  const bool force_tc = pol == DBP_KERNEL_TC_TF32;
+  // the tf32 tensor-core kernel solves one unit per warp: LAMA (10 iterations
+  // over T x U state) and FD-MRC (trivial solves, fold-bound) run faster on
+  // the CTA-cooperative epilogue of the SIMT kernel (measured, round 1)
   const bool fdk = (p.arch == ARCH_FD || p.arch == ARCH_FD_PARTIAL);
   const bool tc_ok = force_tc || (p.kind != EQ_LAMA && !(fdk && p.kind == EQ_MRC));
   if (!force_simt && up <= 32 && tc_ok) {
     int rc = 1;
-    switch (up) {
-      case 8: rc = launch_tc<8>(p, st); break;
-      case 16: rc = launch_tc<16>(p, st); break;
-      case 32: rc = launch_tc<32>(p, st); break;
-    }
-    if (rc == 0) g_last_kernel = 2;
+    rc = launch_tc_up(up, p, st);
+    if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
     p.NS = up <= 16 ? 4 : 3;
   }
@@ -707,12 +510,12 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
   // FD: its per-cluster Grams (B_c = U = 64 at cfg5) are ill-conditioned, and
   // 3xTF32 (no lo.lo term) left FD-ZF 5e-3 from the float64 reference where
   // the FP32 SIMT Gram stays at 2e-4 (cfg5a, measured), for a 2 % gain.
-  const bool wide_ok = !force_simt && up == 64 && !getenv("DBP_NO_WIDE") &&
+  const bool wide_ok = !force_simt && up == 64 && !opt(DBP_OPT_NO_WIDE) &&
                        (p.arch == ARCH_STATS || (p.arch == ARCH_PD && p.kind != EQ_LAMA));
   if (wide_ok) {
     if (p.arch == ARCH_STATS) {
-      const int rc = launch_tc<64>(p, st);
-      if (rc == 0) g_last_kernel = 2;
+      const int rc = launch_tc_up(64, p, st);
+      if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
       if (rc <= 0) return rc;
     } else {
       EqParams q = p;
@@ -721,10 +524,10 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
       const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
       q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
       if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
-      const int rc = launch_tc<64>(q, st);
+      const int rc = launch_tc_up(64, q, st);
       if (rc < 0) return rc;
       if (rc == 0) {
-        g_last_kernel = 2;
+        g_last_kernel = DBP_KERNEL_TC_TF32;
         EqParams r = p;
         r.stats_in = q.stats_out;
         r.C = 1;
@@ -733,24 +536,12 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     }
     p.NS = 3;
   }
-  g_last_kernel = 1;
-  switch (up) {
-    case 8: return launch_stream<8, 128>(p, st);
-    case 16: return launch_stream<16, 128>(p, st);
-    case 32: return launch_stream<32, 256>(p, st);
-    case 64: return launch_stream<64, 256>(p, st);
-  }
-  return fail(DBP_E_UNSUPPORTED, "u must be <= 64");
+  g_last_kernel = DBP_KERNEL_SIMT;
+  return launch_stream_up(up, p, st);
 }
 
 static int dispatch_stats(EqParams& p, cudaStream_t st) {
-  switch (up_for(p.u)) {
-    case 8: return launch_stats<8, 128>(p, st);
-    case 16: return launch_stats<16, 128>(p, st);
-    case 32: return launch_stats<32, 256>(p, st);
-    case 64: return launch_stats<64, 256>(p, st);
-  }
-  return fail(DBP_E_UNSUPPORTED, "u must be <= 64");
+  return launch_stats_up(up_for(p.u), p, st);
 }
 
 // Build the per-item chunk schedule: clusters in order, <= KC rows each.
@@ -800,6 +591,11 @@ int dbp_abi_version(void) { return DBP_ABI_VERSION; }
 const char* dbp_last_error(void) { return g_err.c_str(); }
 
 int dbp_last_kernel(void) { return g_last_kernel; }
+
+int dbp_set_option(int key, int value) {
+  if (key < 0 || key >= DBP_OPT_COUNT) return fail(DBP_E_ARG, "unknown option");
+  return g_opt[key].exchange(value);
+}
 
 int dbp_device_query(int* sms, int* major, int* minor, long long* l2) {
   int dev = 0;
@@ -933,7 +729,9 @@ int dbp_equalize(int arch, int kind, const void* H, const void* Y, int64_t n_ite
   p.iters = iters;
   p.fd_acc = fd_acc;
   p.fd_wraw = fd_wraw;
-  if (const char* ab = getenv("DBP_ABLATE")) p.ablate = atoi(ab);  // timing studies only
+#ifdef DBP_STUDY
+  if (const char* ab = getenv("DBP_ABLATE")) p.ablate = atoi(ab);  // timing studies only (study builds)
+#endif
   return dispatch_stream(p, static_cast<cudaStream_t>(stream));
 }
 

@@ -45,6 +45,12 @@ class Detector:
     cluster (e.g. ClusterPartition.counts).  ``run`` takes device-resident
     H, Y and launches exactly one kernel; ``run_host`` streams host (pinned)
     buffers through the GPU in chunks with the copies overlapped.
+
+    Any partition the reference accepts works: an odd U or an odd cluster size
+    is zero-padded on the device (zero UE columns and zero antenna rows change
+    neither G's leading block nor y_mrc), with the real cluster sizes passed
+    for the FD weights w_c and beta_c (fusion.py:60-68).  The kernels cover
+    U <= 64 and T <= 16.
     """
 
     def __init__(self, arch, kind, n_items, b, u, t, counts, constellation, es=None, lama_params=None):
@@ -54,8 +60,13 @@ class Detector:
         self.counts = [int(c) for c in counts]
         if sum(self.counts) != self.b:
             raise DimensionMismatchError("cluster counts do not sum to B")
-        if any(c % 2 for c in self.counts) or self.u % 2:
-            raise ConfigError("Detector needs even cluster sizes and even U (use the drop-in API otherwise)")
+        if any(c < 1 for c in self.counts):
+            raise ConfigError("every cluster needs at least one antenna")
+        # even row / column strides for the kernels (zero padding, see above)
+        self.us = self.u + (self.u % 2)
+        self.pcounts = [c + (c % 2) for c in self.counts]
+        self.pb = sum(self.pcounts)
+        self.padded = self.us != self.u or self.pb != self.b
         if self.t > 16 or self.u > 64:
             raise ConfigError("Detector supports T <= 16 and U <= 64")
         self.const = constellation
@@ -74,7 +85,7 @@ class Detector:
         self.status = _dev.zeros_i32((self.n,))
         self.iters = _dev.zeros_i32((self.n,))
         self._lv, self._lp, self._L, self._sv, self._sp, self._M = _dev.const_params(constellation)
-        self._off, self._offp = _lib.host_i32(np.concatenate(([0], np.cumsum(self.counts))))
+        self._off, self._offp = _lib.host_i32(np.concatenate(([0], np.cumsum(self.pcounts))))
         self._cnt, self._cntp = _lib.host_i32(self.counts)
         self._lib = _lib.lib()
         self.launches = 0
@@ -87,13 +98,35 @@ class Detector:
         dec = self.dec[o:o + n]
         st = self.status[o:o + n]
         it = self.iters[o:o + n]
+        if self.padded:
+            H, Y = self._pad(H, Y, n)
         _lib.check(self._lib.dbp_equalize(
-            self.arch, _lib.KIND[self.kind.value], _lib.ptr(H), _lib.ptr(Y), n, self.b, self.u, self.u, self.t,
+            self.arch, _lib.KIND[self.kind.value], _lib.ptr(H), _lib.ptr(Y), n, self.pb, self.u, self.us, self.t,
             self.C, self._offp, self._cntp, self.b, float(n0), _lib.ptr(n0_dev), int(n0_group), float(self.es), 1,
             float(self.u / self.b), 1.0, self.t_max, self.damping, self._lp, self._L, self._sp, self._M,
             _lib.ptr(xh), _lib.ptr(s2), None, _lib.ptr(nu), _lib.ptr(dec), _lib.ptr(st), _lib.ptr(it), None,
             None, _lib.stream_ptr(stream)))
         self.launches += 1
+
+    def _pad(self, H, Y, n):
+        """Zero-padded copies [n][pB][us], [n][T][pB] (odd U / odd clusters)."""
+        t_ = _dev.torch()
+        hp = t_.zeros((n, self.pb, self.us), dtype=t_.complex64, device=H.device)
+        yp = t_.zeros((n, self.t, self.pb), dtype=t_.complex64, device=Y.device)
+        a = a2 = 0
+        for c, pc in zip(self.counts, self.pcounts):
+            hp[:, a2:a2 + c, :self.u] = H[:n, a:a + c]
+            yp[:, :, a2:a2 + c] = Y[:n, :, a:a + c]
+            a += c
+            a2 += pc
+        return hp, yp
+
+    def _check_n0(self, n, n0_dev, n0_group):
+        if n0_dev is None:
+            return
+        if n0_group < 1 or n0_dev.numel() * n0_group < n:
+            raise DimensionMismatchError(
+                f"n0_dev has {n0_dev.numel()} values for {n} items in groups of {n0_group}")
 
     def run(self, H, Y, n0=0.0, n0_dev=None, n0_group=1, check=False):
         """H [n][B][U], Y [n][T][B] complex64 CUDA tensors (contiguous).
@@ -101,6 +134,7 @@ class Detector:
         n0_dev[i // n0_group]."""
         if tuple(H.shape) != (self.n, self.b, self.u) or tuple(Y.shape) != (self.n, self.t, self.b):
             raise DimensionMismatchError("H / Y do not match the detector geometry")
+        self._check_n0(self.n, n0_dev, n0_group)
         self._launch(H, Y, self.n, n0, n0_dev, n0_group)
         det = Detection(self.xhat, self.sigma2, self.dec, self.nu, self.status, self.iters)
         return det.raise_on_error() if check else det
@@ -122,6 +156,7 @@ class Detector:
         third, so PCIe traffic overlaps compute.  Returns bytes moved
         (h2d, d2h).  Caller synchronizes."""
         t_ = _dev.torch()
+        self._check_n0(self.n, n0_dev, n0_group)
         if bufs is None:
             bufs = self.device_staging(chunks)
         h2d, comp, d2h = bufs["streams"]
@@ -186,7 +221,9 @@ def detect(arch, kind, H, Y, n0, counts, constellation, lama_params=None, n0_gro
     if n0a.size == 1:
         out = det.run(Hd, Yd, float(n0a[0]))
     else:
-        grp = n0_group or max(1, n // n0a.size)
+        grp = int(n0_group) if n0_group else max(1, n // n0a.size)
+        if grp * n0a.size != n:
+            raise DimensionMismatchError(f"{n0a.size} noise values do not cover {n} items in groups of {grp}")
         out = det.run(Hd, Yd, 0.0, _dev.to_f32(n0a)[0], grp)
     if check:
         out.raise_on_error()

@@ -9,6 +9,7 @@ import pytest
 import paper_1808_04473_b200 as dbp
 from paper_1808_04473_b200 import (ClusterPartition, ConfigError, DivergenceError, FusedStats, SingularGramError,
                                    SystemConfig)
+from paper_1808_04473_b200.equalize import EqualizerOutput
 from paper_1808_04473_b200.fusion import ClusterOutput, FusionWeights
 from oracle import dbp_oracle as O
 
@@ -368,24 +369,45 @@ class TestFuseEstimates:
             dbp.fuse_estimates(outs, FusionWeights(nu=np.ones((3, 1)) / 3))
 
 
+class TestNegativeVariance:
+    """equalize.py:115-120 on the device: unbiased_output's variance
+    (sigma2 - (1 - c)^2 Es) / c^2 below -1e-9 raises NegativeVarianceError
+    (status ST_NEGVAR of dbp_unbias), rounding-level negatives clamp to 0."""
+
+    def test_unbias_negative_variance_raises(self):
+        out = EqualizerOutput(z=np.array([1 + 0j, 0.5j]), sigma2=np.array([0.3, 0.01]), equalizer=dbp.Equalizer.LMMSE,
+                              signal_gain=np.array([0.9, 0.5]))
+        with pytest.raises(dbp.NegativeVarianceError):
+            dbp.unbiased_output(out)
+
+    def test_unbias_rounding_negative_clamps(self):
+        c = 0.5
+        out = EqualizerOutput(z=np.array([1 + 0j]), sigma2=np.array([np.nextafter(np.float32((1 - c) ** 2), np.float32(0))]), equalizer=dbp.Equalizer.LMMSE,
+                              signal_gain=np.array([c]))
+        res = dbp.unbiased_output(out)
+        assert res.sigma2[0] == 0.0
+
+
 class TestFdPipeline:
     def test_golden_units(self, golden):
         g = golden("units")
         for c in (1, 2, 4, 8):
             part = ClusterPartition.uniform(64, c)
             ch = dbp.ChannelRealization(g[f"fd{c}_h"], part)
-            # fp32 error grows with the local condition number (square local
-            # systems, B_c = U = 16 at C = 4, reach kappa(G_c) ~ 4e4): tolerance
-            # max(1e-4, 2e-6 kappa_max) -- the BASELINE configs have kappa ~ 20
+            # MRC, L-MMSE (regularized: kappa(G_c + rho I) <= 1 + ||G_c|| / rho)
+            # and LAMA (no inverse) are held to the fixed 1e-4 of the north
+            # star.  Only unregularized ZF on a square local system (B_c = U =
+            # 16 at C = 4: kappa(G_c) ~ 4e4) gets an allowance proportional to
+            # kappa; C = 8 (B_c < U) has no ZF case (SingularGramError).
             hh = g[f"fd{c}_h"]
             kappa = max(np.linalg.cond(hh[sl].conj().T @ hh[sl]) for sl in part.slices())
-            tol = max(1e-4, 2e-6 * kappa)
             for kind in ("mrc", "zf", "lmmse", "lama"):
                 if f"fd{c}_{kind}_z" not in g:
                     continue
                 lp = {"t_max": 5} if kind == "lama" else None
                 fd = dbp.fd_equalize(kind, ch, g[f"fd{c}_y"], 0.1, constellation=QAM16, lama_params=lp,
                                      return_weights=True)
+                tol = max(1e-4, 2e-6 * kappa) if (kind == "zf" and 64 // c <= 16) else 1e-4
                 assert rel(fd.z, g[f"fd{c}_{kind}_z"]) < tol, (c, kind)
                 assert rel(fd.sigma2, g[f"fd{c}_{kind}_sigma2"]) < tol, (c, kind)
                 assert rel(fd.nu, g[f"fd{c}_{kind}_nu"]) < tol, (c, kind)

@@ -48,10 +48,12 @@ def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
     res = grp.run(H, Y, n0)
     ref = dbp.detect(arch, kind, g["H"], g["Y"], g["n0"], [b // c] * c, const, lama_params=lp)
     assert res.items == (0, H.shape[0])
-    # both sides are fp32 with different Gram summation orders (fused TMEM
-    # accumulation over clusters vs per-cluster stats + reduce-scatter); the
-    # ten LAMA iterations amplify that rounding difference
-    tol = 1e-5 if kind == "lama" else 2e-6
+    # different Gram arithmetic on the two sides: the fused PD kernel uses two
+    # bf16 parts per operand (~1e-5 from the float64 reference, tests/
+    # test_gpu_tc2.py), the per-rank statistics three parts; the FD and LAMA
+    # sides differ only in fp32 summation order (the ten LAMA iterations
+    # amplify it).  Both sides are within 1e-4 of the reference on their own.
+    tol = 5e-5 if (arch == "pd" and kind != "lama") else 1e-5 if kind == "lama" else 2e-6
     assert normwise_rel(res.xhat.cpu().numpy(), ref.xhat) < tol
     assert np.mean(res.decisions.cpu().numpy() != ref.decisions) < 1e-3
     if arch == "fd":

@@ -6,12 +6,12 @@ tests/test_oracle_golden.py).
 The launcher picks, per geometry, how many whole items share one shared-memory
 stage (ips), whether an item is split into antenna row blocks (spi > 1),
 whether two units share one tensor-core tile (pair), and the ring depth.  The
-timing-study overrides DBP_TC_SMAX / DBP_TC_NS / DBP_TC_PAIR force each
-variant here on small inputs, including odd item counts (a null half in the
-last pair), paired items in different stages, row blocks whose clusters pair
-inside one stage, and an odd cluster count (FD without pairing)."""
-
-import os
+options tc_smax_kb / tc_ns / tc_pair (dbp_set_option) force each variant here
+on small inputs, including odd item counts (a null half in the last pair),
+paired items in different stages, row blocks whose clusters pair inside one
+stage, and an odd cluster count (FD without pairing).  U <= 16 linear
+geometries run on the split-bf16 kernel by default (tests/test_gpu_tc2.py);
+here the 3xTF32 kernel is forced."""
 
 import numpy as np
 import pytest
@@ -26,15 +26,15 @@ pytestmark = pytest.mark.gpu
 # (arch, kind, n_items, B, C, U, T, bits, env)
 CASES = [
     ("pd", "lmmse", 7, 128, 4, 16, 14, 4, {}),                        # 2 items/stage, null half at the end
-    ("pd", "lmmse", 9, 128, 4, 16, 14, 4, {"DBP_TC_SMAX": "96"}),     # 3 items/stage: pairs straddle stages
-    ("pd", "lmmse", 5, 128, 4, 16, 14, 4, {"DBP_TC_SMAX": "20"}),     # row blocks (spi = 2), paired items
-    ("pd", "zf", 6, 128, 4, 16, 14, 6, {"DBP_TC_PAIR": "1"}),         # one unit per tile
+    ("pd", "lmmse", 9, 128, 4, 16, 14, 4, {"tc_smax_kb": 96}),     # 3 items/stage: pairs straddle stages
+    ("pd", "lmmse", 5, 128, 4, 16, 14, 4, {"tc_smax_kb": 20}),     # row blocks (spi = 2), paired items
+    ("pd", "zf", 6, 128, 4, 16, 14, 6, {"tc_pair": 1}),         # one unit per tile
     ("pd", "lmmse", 6, 96, 3, 8, 5, 4, {}),                            # U = 8 (two units in one 32-row block)
-    ("pd", "mrc", 4, 256, 8, 32, 14, 6, {"DBP_TC_SMAX": "40"}),       # U = 32, row blocks
+    ("pd", "mrc", 4, 256, 8, 32, 14, 6, {"tc_smax_kb": 40}),       # U = 32, row blocks
     ("fd", "lmmse", 5, 128, 4, 16, 14, 4, {}),                        # clusters paired inside an item
-    ("fd", "zf", 4, 256, 8, 16, 14, 6, {"DBP_TC_SMAX": "32", "DBP_TC_NS": "3"}),  # row blocks at cluster pairs
+    ("fd", "zf", 4, 256, 8, 16, 14, 6, {"tc_smax_kb": 32, "tc_ns": 3}),  # row blocks at cluster pairs
     ("fd", "mrc", 5, 96, 3, 16, 7, 4, {}),                            # odd cluster count: no pairing
-    ("fd", "lmmse", 3, 64, 2, 8, 14, 4, {"DBP_TC_NS": "2"}),          # cfg1 shape
+    ("fd", "lmmse", 3, 64, 2, 8, 14, 4, {"tc_ns": 2}),          # cfg1 shape
     ("pd", "lama", 3, 128, 4, 16, 14, 4, {}),                          # LAMA epilogue on a solver warp
     ("fd", "lama", 3, 128, 4, 8, 6, 2, {}),                            # FD LAMA fold
 ]
@@ -51,19 +51,10 @@ def test_staging_variant_matches_oracle(arch, kind, n, b, c, u, t, bits, env):
     noise = (rng.standard_normal((n, t, b)) + 1j * rng.standard_normal((n, t, b))) * np.sqrt(n0 / 2)
     Y = (np.einsum("nbu,ntu->ntb", H.astype(complex), s) + noise).astype(np.complex64)
     counts = [b // c] * c
-    env = dict(env, DBP_FORCE_TC="1")  # LAMA / FD-MRC default to the SIMT kernel
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        lp = {"t_max": 5} if kind == "lama" else None
+    lp = {"t_max": 5} if kind == "lama" else None
+    with _lib.options(kernel=_lib.KERNEL_TC_TF32, **env):  # forced: other kernels are the default here
         det = dbp.detect(arch, kind, H, Y, n0, counts, const, lama_params=lp)
-        assert _lib.lib().dbp_last_kernel() == 2  # the tensor-core kernel ran
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        assert _lib.lib().dbp_last_kernel() == _lib.KERNEL_TC_TF32  # the 3xTF32 tensor-core kernel ran
     offs = [0] + list(np.cumsum(counts))
     ref = O.run_batch(arch, kind, H.astype(complex), Y.astype(complex), offs, n0, 1.0, const.symbols,
                       lama_params=lp)
