@@ -24,3 +24,17 @@ clean:
 	rm -rf build $(LIB) build_ptxas.log
 
 .PHONY: all clean
+
+# study build (timing ablations via DBP_ABLATE, debug counters; never the
+# shipped library): make study [SUFFIX=_x EXTRA="-DDBP_T2_NSET=3"] ->
+# build_study_x/libdbp_study.so; load it with DBP_LIB
+SDIR := build_study$(SUFFIX)
+STUDY_OBJS := $(patsubst $(CSRC)/%.cu,$(SDIR)/%.o,$(SRCS))
+STUDY_LIB := $(SDIR)/libdbp_study.so
+$(SDIR)/%.o: $(CSRC)/%.cu $(HDR)
+	@mkdir -p $(SDIR)
+	$(NVCC) $(NVFLAGS) -DDBP_STUDY $(EXTRA) -c -o $@ $< 2> $(SDIR)/$*.ptxas.log || (cat $(SDIR)/$*.ptxas.log; exit 1)
+$(STUDY_LIB): $(STUDY_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(STUDY_OBJS) -lcudart
+study: $(STUDY_LIB)
+.PHONY: study

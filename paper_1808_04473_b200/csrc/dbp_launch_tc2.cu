@@ -35,7 +35,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <int MODE, int NSPLIT>
 static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm, const CUtensorMap& ym,
                            cudaStream_t st) {
-  const bool fd = MODE == T2_FD;
+  const bool fd = MODE == T2_FD || MODE == T2_FD_MRC;
   const Tc2Layout L = make_tc2_layout(g, p.TP, p.C, fd);
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
@@ -46,7 +46,28 @@ static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm,
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int gpi = g.upi > 4 ? g.upi / 4 : 1;  // groups per item (CTAs own whole items)
   const int64_t grid = std::min<int64_t>(g.G_tot / gpi, (int64_t)sm_count());
+#ifdef DBP_STUDY
+  static long long* dbg = nullptr;
+  const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
+  if (debug) {
+    if (!dbg) cudaMalloc(&dbg, 64 * 4 * sizeof(long long));
+    cudaMemsetAsync(dbg, 0, 64 * 4 * sizeof(long long), st);
+    p.dbg = dbg;
+  }
+#endif
   kern<<<(unsigned)grid, T2_THREADS, L.total, st>>>(p, hm, ym, g);
+#ifdef DBP_STUDY
+  if (debug) {
+    long long h[64 * 4];
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[tc2 debug] NS=%d stage=%d (mean cycles per CTA)\n", g.NS, g.stage_bytes);
+    for (int w = 0; w < T2_THREADS / 32; ++w) {
+      const char* name = w == 0 ? "producer" : w == 1 ? "mma" : w < T2_FIRST_SOLV ? "converter" : "solver";
+      fprintf(stderr, "  w%-2d %-9s total %9.0f  wait1 %9.0f  wait2 %9.0f\n", w, name, (double)h[w * 4] / grid,
+              (double)h[w * 4 + 1] / grid, (double)h[w * 4 + 2] / grid);
+    }
+  }
+#endif
   return cuda_check("tc2_kernel");
 }
 
@@ -82,6 +103,7 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   g.U_tot = p.n_items * upi;
   g.G_tot = (g.U_tot + 3) / 4;
   g.hbytes = 4 * 32 * 2 * p.us * 4;
+  g.lean = (p.kind == EQ_MRC && p.arch != ARCH_STATS) ? 2 : 1;
   g.ybox = g.gn * p.T * T2_YROW * 4;
   g.ystride = align_up(g.ybox, 128);
   const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : (p.arch == ARCH_PD) ? 2 : 3;
@@ -127,7 +149,14 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   }
   if (p.arch == ARCH_STATS) return nsplit == 2 ? launch_tc2_mode<T2_STATS, 2>(p, g, hm, ym, st)
                                                : launch_tc2_mode<T2_STATS, 3>(p, g, hm, ym, st);
-  if (fdm) return nsplit == 2 ? launch_tc2_mode<T2_FD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3>(p, g, hm, ym, st);
+  const bool mrc = p.kind == EQ_MRC;
+  if (fdm) {
+    if (mrc) return nsplit == 2 ? launch_tc2_mode<T2_FD_MRC, 2>(p, g, hm, ym, st)
+                                : launch_tc2_mode<T2_FD_MRC, 3>(p, g, hm, ym, st);
+    return nsplit == 2 ? launch_tc2_mode<T2_FD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3>(p, g, hm, ym, st);
+  }
+  if (mrc) return nsplit == 2 ? launch_tc2_mode<T2_PD_MRC, 2>(p, g, hm, ym, st)
+                              : launch_tc2_mode<T2_PD_MRC, 3>(p, g, hm, ym, st);
   return nsplit == 2 ? launch_tc2_mode<T2_PD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_PD, 3>(p, g, hm, ym, st);
 }
 

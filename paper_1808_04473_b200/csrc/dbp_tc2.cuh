@@ -35,13 +35,35 @@
 //   warp 1          MMA issuer (one thread): NSPLIT-products x 2 K-steps per
 //                   stage into accumulator (group & 1) (2 x 256 TMEM columns)
 //   warps 2..       converters (T2_NCONV warps)
-//   then            solvers: T2_NSET sets of 4 warps; set s takes groups
-//                   s, s + NSET, ...; warp (s, q) reads unit q's 32 lanes x
-//                   64 columns, releases the accumulator, recombines G / y_mrc
-//                   into its shared-memory work area and runs the unit
-//                   epilogue (dbp_epilogue.cuh).
+//   then            8 solvers in 2 sets; set s owns accumulator s (groups
+//                   s, s + 2, ...); per pass warp (s, q) reads unit q of
+//                   groups g and g + 2 -- 32 lanes x 64 columns each --
+//                   releasing the accumulator right after each read,
+//                   recombines G / y_mrc into its two shared-memory work areas
+//                   and solves the two units on its two half-warps
+//                   (t2_solve_pair), writing the outputs (PD) or the FD fold
+//                   records directly.
+//   The producer also prefetches the stages NS ahead into L2
+//   (cp.async.bulk.prefetch.tensor), so a stage that frees up is refilled
+//   from L2 rather than DRAM.
 #pragma once
 #include <cuda.h>
+
+// timing-study ablations (study builds only: make study): 1 solvers skip the
+// epilogue, 2 no MMAs, 4 converters skip the conversion
+#ifdef DBP_STUDY
+#define T2_ABLATE(bit) (p.ablate & (bit))
+// per-warp wait-cycle counters (DBP_TC_DEBUG): [warp][total, wait1, wait2, -]
+#define T2_WAIT(bar, par, slot)           \
+  do {                                    \
+    const long long t0_ = clock64();      \
+    mbar_wait(bar, par);                  \
+    dbgc[slot] += clock64() - t0_;        \
+  } while (0)
+#else
+#define T2_ABLATE(bit) false
+#define T2_WAIT(bar, par, slot) mbar_wait(bar, par)
+#endif
 
 #include "dbp_tc.cuh"
 
@@ -50,21 +72,20 @@ namespace dbp {
 #ifndef DBP_T2_NCONV
 #define DBP_T2_NCONV 4
 #endif
-#ifndef DBP_T2_NSET
-#define DBP_T2_NSET 2
-#endif
 constexpr int T2_NCONV = DBP_T2_NCONV;               // converter warps
-constexpr int T2_NSET = DBP_T2_NSET;                 // solver sets (4 warps each)
 constexpr int T2_FIRST_CONV = 2;
 constexpr int T2_FIRST_SOLV = T2_FIRST_CONV + T2_NCONV;
-constexpr int T2_NSOLV = 4 * T2_NSET;
+constexpr int T2_NSOLV = 8;                          // solver warps: 2 sets x 4 TMEM lane quarters
+constexpr int T2_NWORK = 2 * T2_NSOLV;               // work areas: two units in flight per solver warp
 constexpr int T2_THREADS = 32 * (T2_FIRST_SOLV + T2_NSOLV);
 constexpr int T2_CT = 32 * T2_NCONV;                 // converter threads
 constexpr int T2_YROW = 68;                          // floats per staged Y row (64 + 4 pad)
 constexpr int T2_SPLIT_BYTES = 16384;                // one bf16 split of a stage tile
 constexpr int T2_FD_CNT = 64;
 
-enum { T2_STATS = 0, T2_PD = 1, T2_FD = 2 };
+// one kernel per epilogue class, so each binary carries only its own solver
+// code (instruction-cache footprint)
+enum { T2_STATS = 0, T2_PD = 1, T2_FD = 2, T2_PD_MRC = 3, T2_FD_MRC = 4 };
 
 // Geometry of one launch (host-computed).
 struct Tc2Geom {
@@ -79,6 +100,7 @@ struct Tc2Geom {
   int hbytes;   // bytes of the H box (4 units x 32 x 2us floats)
   int ybox;     // bytes of one Y box (gn items x T rows x 68 floats)
   int ystride;  // shared-memory stride between the Y boxes (128-byte aligned)
+  int lean;     // compact solver work areas: 1 = t2_solve_pair / statistics, 2 = MRC
   int64_t U_tot;  // units in the launch
   int64_t G_tot;  // groups in the launch
 };
@@ -102,8 +124,34 @@ __host__ __device__ inline Tc2Layout make_tc2_layout(const Tc2Geom& g, int TP, i
   o += g.NS * g.stage_bytes;
   L.work = o;
   L.w = make_work_layout(0, 16, TP, C, false, fd);
+  if (g.lean) {  // only what the kernel's epilogue touches (smem for the stage ring)
+    const int LD = 16 + 2;
+    int q = 0;
+    L.w.G = q;
+    q += 16 * LD * 8;
+    L.w.Z = q;
+    q += TP * LD * 8;
+    L.w.Sv = L.w.Vv = L.w.Fb = L.w.gb = L.w.num = L.w.phi = L.w.coef = L.w.den = L.w.harm = L.w.wbuf = L.w.Z;
+    if (g.lean == 2) {  // MRC team epilogue: estimates, variances, gains
+      L.w.X = q;
+      q += TP * LD * 8;
+      L.w.s2 = q;
+      q += 16 * 4;
+      L.w.gn = q;
+      q += 16 * 4;
+      L.w.dg = q;
+      q += 16 * 4;
+      L.w.W = L.w.Z;
+    } else {  // t2_solve_pair / statistics: the pivot-column buffers
+      L.w.W = q;
+      q += 32 * 8;
+      L.w.X = L.w.s2 = L.w.gn = L.w.dg = L.w.Z;
+    }
+    L.w.flags = q;
+    L.w.total = align_up(q + 16, 128);
+  }
   L.work_stride = L.w.total;
-  o += T2_NSOLV * L.work_stride;
+  o += T2_NWORK * L.work_stride;
   L.total = align_up(o, 128);
   return L;
 }
@@ -124,6 +172,16 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "{%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -171,23 +229,35 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // bf16 splits of a float pair (x0 at the lower address): h = rn(x), m =
-// rn(x - h) (, l = rn(x - h - m)); returns packed bf16x2 words
+// rn(x - h) (, l = rn(x - h - m)); returns packed bf16x2 words.  The residual
+// of the pair is one packed FP32 subtraction (FADD2, sm_100).
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf2_rn(uint64_t x) {  // {lo float, hi float} -> bf16x2
+  uint32_t h;
+  asm("{\n\t.reg .f32 a, b;\n\tmov.b64 {a, b}, %1;\n\tcvt.rn.bf16x2.f32 %0, b, a;\n\t}" : "=r"(h) : "l"(x));
+  return h;
+}
+__device__ __forceinline__ uint64_t bf2_unpack(uint32_t h) {  // bf16x2 -> {lo float, hi float}
+  return f2_pack(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+}
 template <int NSPLIT>
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t (&w)[NSPLIT]) {
-  uint32_t h;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+  const uint64_t x = f2_pack(x0, x1);
+  const uint32_t h = bf2_rn(x);
   w[0] = h;
-  float r0 = x0 - __uint_as_float(h << 16), r1 = x1 - __uint_as_float(h & 0xffff0000u);
-  uint32_t m;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(m) : "f"(r1), "f"(r0));
+  const uint64_t r = f2_sub(x, bf2_unpack(h));
+  const uint32_t m = bf2_rn(r);
   w[1] = m;
-  if constexpr (NSPLIT == 3) {
-    r0 -= __uint_as_float(m << 16);
-    r1 -= __uint_as_float(m & 0xffff0000u);
-    uint32_t l;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r1), "f"(r0));
-    w[2] = l;
-  }
+  if constexpr (NSPLIT == 3) w[2] = bf2_rn(f2_sub(r, bf2_unpack(m)));
 }
 
 // byte offset of MN element e (multiple of 8 / 4) of MN block b, K row k
@@ -195,12 +265,198 @@ __device__ __forceinline__ int t2_off(int b, int k, int e) {
   return b * 4096 + k * 128 + ((((e >> 3) ^ (k & 7))) << 4) + (e & 7) * 2;
 }
 
+// ---- solver of the split-bf16 kernel --------------------------------------
+// Nearest symbol (equalize.py:262-268): per-dimension PAM slicer for square
+// QAM (ties to the lower level), generic set otherwise; a short runtime loop
+// (compact code: the solver shares the instruction cache with the other roles)
+__device__ __forceinline__ int t2_slice(float2 z, const ConstParams& cp) {
+  if (cp.L == 0) return slice_symbol(z, cp);
+  int i = 0, j = 0;
+#pragma unroll 1
+  for (int l = 0; l < cp.L - 1; ++l) {
+    const float mid = cp.mids[l];
+    i += (z.x > mid) ? 1 : 0;
+    j += (z.y > mid) ? 1 : 0;
+  }
+  return i * cp.L + j;
+}
+
+// Two units per warp, one per half-warp (ZF / L-MMSE, equalize.py:153-172 +
+// unbiased_output :179-195).  Lane (h = lane / 16, j = lane % 16) owns column
+// j of unit h's matrix M = G + rho I (all 16 rows in registers).  In-place
+// Gauss-Jordan inverse without pivoting (M is Hermitian positive definite),
+// written as the branch-free rank-1 update  m_ij -= c_i r_j  with
+//   c_i = M_ik (i != k), c_k = p - 1;   r_j = M_kj / p (j != k), r_k = 1 + 1/p
+// (which yields M_kj/p on the pivot row, -M_ik/p on the pivot column, 1/p on
+// the pivot).  r_j is the lane's own element; the pivot column is published
+// by lane k through a double-buffered shared-memory column and read back as
+// broadcasts.  A = M^-1 is Hermitian, so lane j also holds row j of A
+// (conjugated): x_t[j] = sum_i conj(A_ij) y_t[i], sigma2 = N0 A_jj,
+// c = 1 - rho A_jj, unbiased z / c and N0 A_jj / c.  Outputs go straight to
+// x-hat / decisions / sigma2 / status (PD) or to the cluster's fold record
+// (FD).  A pivot below 8 u eps of its original diagonal is SingularGramError
+// (the fp32 counterpart of zpotrf's "not positive definite").
+template <bool FD>
+__device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
+                              const bool* valid, int lane) {
+  const int h = lane >> 4, j = lane & 15;
+  const int u = p.u, T = p.T, LD = w[0].LD;
+  const bool lmmse = p.kind == EQ_LMMSE;
+  const bool act = h ? valid[1] : valid[0];
+  const int64_t nh = h ? n[1] : n[0];
+  const int ch = h ? c[1] : c[0];
+  const float n0h = h ? n0[1] : n0[0];
+  const float2* G = h ? w[1].G : w[0].G;
+  const float2* Z = h ? w[1].Z : w[0].Z;
+  float2* colb = h ? w[1].W : w[0].W;  // [2][16] pivot columns (double-buffered)
+  const float rho = lmmse ? n0h / p.es : 0.f;
+  float2 m[16];
+  float dg = 1.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding (u < 16, idle half): identity
+    if (act && i < u && j < u) {
+      v = G[i * LD + j];
+      if (i == j) {
+        v.x += rho;
+        v.y = 0.f;
+        dg = v.x;
+      }
+    }
+    m[i] = v;
+  }
+  const float tolf = 8.f * (float)u * FLT_EPSILON;
+  bool bad = false;
+  // Rotating register order: at step k the lane's row-k element is m[k % 4]
+  // of the current frame, and after every 4 steps the registers rotate by 4,
+  // so all indices stay static with a 4-step unrolled body; the pivot column
+  // is published and read in the same frame.  Padded steps (k >= u) are
+  // identity pivots and no-ops, but are kept so that the frame returns to
+  // the original order after 16 steps.
+#pragma unroll 1
+  for (int k0 = 0; k0 < 16; k0 += 4) {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk;
+      float2* cb = colb + (kk & 1) * 16;
+      if (j == k) {  // publish the pivot column (a failed pivot is replaced by 1)
+        float2 pk = m[kk];
+        if (act && k < u && !(pk.x > tolf * dg)) {
+          bad = true;
+          pk = make_float2(1.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float2 a0 = (i == kk) ? pk : m[i], a1 = (i + 1 == kk) ? pk : m[i + 1];
+          *reinterpret_cast<float4*>(cb + i) = make_float4(a0.x, a0.y, a1.x, a1.y);
+        }
+      }
+      __syncwarp();
+      float2 cc[16];
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const float4 v = *reinterpret_cast<const float4*>(cb + i);
+        cc[i] = make_float2(v.x, v.y);
+        cc[i + 1] = make_float2(v.z, v.w);
+      }
+      const float pv = cc[kk].x;
+      const float rp = __frcp_rn(pv);
+      const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[kk], rp);
+      cc[kk] = make_float2(pv - 1.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
+    }
+    float2 t4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t4[i] = m[i];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
+  }
+  const unsigned bm = __ballot_sync(0xffffffffu, bad);
+  float ajj = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i == j) ajj = m[i].x;
+  const bool unb = lmmse && (FD || p.unbias);
+  const float cgain = 1.f - rho * ajj;
+  const float sc = unb ? __frcp_rn(cgain) : 1.f;
+  const bool badc = act && j < u && unb && !(cgain > 0.f);
+  const unsigned bc = __ballot_sync(0xffffffffu, badc);
+  const int st = (((bm | bc) >> (16 * h)) & 0xffffu) ? ST_SINGULAR : ST_OK;
+  float* rec = nullptr;
+  if constexpr (FD) rec = p.fd_scratch + ((size_t)nh * p.C + ch) * fd_record_floats(u, T, u);
+  if (act && j < u) {
+    for (int t = 0; t < T; t += 2) {  // symbols t, t + 1: four independent chains
+      const int t1 = (t + 1 < T) ? t + 1 : t;
+      const float2* z0 = Z + t * LD;
+      const float2* z1 = Z + t1 * LD;
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+#pragma unroll
+      for (int i0 = 0; i0 < 16; i0 += 8) {  // half a row of loads in flight at a time
+        if (i0 >= u) break;
+        float4 y0[4], y1[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = i0 + 2 * e;
+          y0[e] = (i < u) ? *reinterpret_cast<const float4*>(z0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          y1[e] = (i < u) ? *reinterpret_cast<const float4*>(z1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = i0 + 2 * e;
+          // y_t[i] beyond u was never written (zeroed above; its A column is zero)
+          c_fma_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
+          c_fma_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
+          c_fma_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
+          c_fma_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (e == 1 && t + 1 >= T) break;
+        const int te = t + e;
+        const float2 x = c_scale(e ? c_add(b0, b1) : c_add(a0, a1), sc);
+        if constexpr (FD) {
+          reinterpret_cast<float2*>(rec)[te * u + j] = x;
+        } else {
+          const size_t o = ((size_t)nh * T + te) * u + j;
+          p.xhat[o] = x;
+          if (p.dec) p.dec[o] = (uint8_t)t2_slice(x, p.cp);
+        }
+      }
+    }
+    const float nv = n0h * ajj;
+    const float s2 = (p.kind == EQ_ZF) ? nv : (unb ? nv / cgain : nv);
+    if constexpr (FD) {
+      rec[2 * T * u + j] = s2;
+    } else {
+      p.sigma2[(size_t)nh * u + j] = s2;
+      if (p.gain && lmmse) p.gain[(size_t)nh * u + j] = cgain;
+    }
+  }
+  if (act && j == 0) {
+    if constexpr (FD) {
+      int* f = reinterpret_cast<int*>(rec + 2 * T * u + 2 * u);
+      f[0] = st;
+      f[1] = 0x7fffffff;
+    } else {
+      p.status[nh] = st;
+      if (p.iters) p.iters[nh] = 0;
+    }
+  }
+}
+
 template <int MODE, int NSPLIT>
-__global__ void __launch_bounds__(T2_THREADS, 1)
+// register cap: a warp lives on one of the 4 SM sub-partitions (16K registers
+// each), which hold ceil(warps / 4) warps
+__global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     tc2_kernel(const __grid_constant__ EqParams p, const __grid_constant__ CUtensorMap hmap,
                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ Tc2Geom g) {
   extern __shared__ __align__(1024) char smem[];
-  constexpr bool fd = (MODE == T2_FD);
+  constexpr bool fd = (MODE == T2_FD || MODE == T2_FD_MRC);
+  constexpr bool mrc = (MODE == T2_PD_MRC || MODE == T2_FD_MRC);
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int NS = g.NS;
   const Tc2Layout L = make_tc2_layout(g, p.TP, p.C, fd);
@@ -230,6 +486,10 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef DBP_STUDY
+  long long dbgc[4] = {0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
 
   // contiguous range of whole items per CTA: blocks of gpi = max(1, upi / 4)
   // groups (groups never straddle items: upi | 4 or 4 | upi), so all clusters
@@ -248,24 +508,40 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
       prefetch_tmap(&hmap);
       prefetch_tmap(&ymap);
       const uint64_t policy = l2_evict_first_policy();
+      const int total = ngroups * nch;
+      // stage sequence number -> (group, chunk) coordinates
+      auto coords = [&](int sq, int& j, int64_t& u0, int& n0, int& c0) {
+        const int gl = sq / nch;
+        j = sq - gl * nch;
+        u0 = (g_first + gl) * 4;
+        n0 = (int)(u0 / g.upi);
+        c0 = (int)(u0 % g.upi);
+      };
+      auto prefetch = [&](int sq) {
+        int j, n0, c0;
+        int64_t u0;
+        coords(sq, j, u0, n0, c0);
+        tma_prefetch_3d(&hmap, 0, 32 * j, (int)u0);
+        for (int cl = 0; cl < g.gc; ++cl) tma_prefetch_4d(&ymap, 64 * j, c0 + cl, 0, n0);
+      };
+      for (int sq = NS; sq < 2 * NS && sq < total; ++sq) prefetch(sq);
       int s = 0;
       uint32_t ph = 0;
-      int sq = 0;
-      for (int gl = 0; gl < ngroups; ++gl) {
-        const int64_t u0 = (g_first + gl) * 4;
-        const int n0 = (int)(u0 / g.upi), c0 = (int)(u0 % g.upi);
-        for (int j = 0; j < nch; ++j, ++sq) {
-          if (sq >= NS) mbar_wait(&stage_empty[s], ph ^ 1u);
-          const uint32_t bar = smem_u32(&raw_full[s]);
-          mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(g.hbytes + g.gc * g.ybox));
-          const uint32_t dst = stg0 + (uint32_t)(s * g.stage_bytes);
-          tma_load_3d(dst, &hmap, 0, 32 * j, (int)u0, bar, policy);
-          for (int cl = 0; cl < g.gc; ++cl)
-            tma_load_4d(dst + g.hbytes + cl * g.ystride, &ymap, 64 * j, c0 + cl, 0, n0, bar, policy);
-          if (++s == NS) {
-            s = 0;
-            ph ^= 1u;
-          }
+      for (int sq = 0; sq < total; ++sq) {
+        if (sq >= NS) T2_WAIT(&stage_empty[s], ph ^ 1u, 1);
+        int j, n0, c0;
+        int64_t u0;
+        coords(sq, j, u0, n0, c0);
+        const uint32_t bar = smem_u32(&raw_full[s]);
+        mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(g.hbytes + g.gc * g.ybox));
+        const uint32_t dst = stg0 + (uint32_t)(s * g.stage_bytes);
+        tma_load_3d(dst, &hmap, 0, 32 * j, (int)u0, bar, policy);
+        for (int cl = 0; cl < g.gc; ++cl)
+          tma_load_4d(dst + g.hbytes + cl * g.ystride, &ymap, 64 * j, c0 + cl, 0, n0, bar, policy);
+        if (sq + 2 * NS < total) prefetch(sq + 2 * NS);  // keep 2 NS stages of lookahead in L2
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
         }
       }
     }
@@ -282,11 +558,11 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
       uint32_t ph = 0;
       for (int gl = 0; gl < ngroups; ++gl) {
         const int a = gl & 1;
-        if (gl >= 2) mbar_wait(&acc_empty[a], (uint32_t)(((gl >> 1) - 1) & 1));
+        if (gl >= 2) T2_WAIT(&acc_empty[a], (uint32_t)(((gl >> 1) - 1) & 1), 2);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(256 * a);
         for (int j = 0; j < nch; ++j) {
-          mbar_wait(&conv_full[s], ph);
+          T2_WAIT(&conv_full[s], ph, 1);
           tc_fence_after();
           const uint32_t base = stg0 + (uint32_t)(s * g.stage_bytes);
 #pragma unroll
@@ -295,7 +571,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
             for (int pr = 0; pr < NP; ++pr) {
               const uint64_t da = umma_desc_mn16(base + PA[pr] * T2_SPLIT_BYTES + ks * 2048);
               const uint64_t db = umma_desc_mn16(base + PB[pr] * T2_SPLIT_BYTES + ks * 2048);
-              umma_bf16(d, da, db, idesc, (j | ks | pr) ? 1u : 0u);
+              if (!T2_ABLATE(2)) umma_bf16(d, da, db, idesc, (j | ks | pr) ? 1u : 0u);
             }
           }
           umma_commit(&stage_empty[s]);
@@ -317,72 +593,74 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
     constexpr int HT = 4 * 32 * 8 / T2_CT;  // H tasks per thread at us = 16
     constexpr int YT = 4 * 16 * 4 / T2_CT;  // Y tasks per thread (T <= 16)
     static_assert(HT * T2_CT == 1024 && YT * T2_CT == 256, "converter task split");
+    // per-thread task tables, the same for every stage (float index of the
+    // load in the stage, byte offset of the store in a split tile)
+    // H task e: quad jq of antenna row k (+4 r) of unit q; 16-lane phases =
+    // 8 quads x rows {k, k + 4} (conflict-free loads and 8-byte stores)
+    int hld[HT], hst[HT];
+#pragma unroll
+    for (int i = 0; i < HT; ++i) {
+      const int e = ct + i * T2_CT;
+      const int jq = e % qpr, e2 = e / qpr;
+      const int r = e2 & 1, kk = (e2 >> 1) & 15, q = e2 >> 5;
+      const int k = (kk & 3) + 8 * (kk >> 2) + 4 * r;
+      hld[i] = (q * 32 + k) * 2 * us + 4 * jq;
+      hst[i] = (e < nh) ? t2_off(q >> 1, k, 32 * (q & 1) + 4 * jq) : -1;
+    }
+    // Y task e: antenna pair kp, symbol block tb (t = 4 tb .. 4 tb + 3) of
+    // unit q; 8-lane phases = 4 antenna pairs x 2 symbol blocks.  The store
+    // for antenna 2kp + 1 sits at the next 128-byte K row, its chunk position
+    // the XOR with (k % 8) flipped in bit 0.
+    int yld[YT], yst0[YT], yst1[YT], yt0[YT];
+#pragma unroll
+    for (int i = 0; i < YT; ++i) {
+      const int e = ct + i * T2_CT;
+      const int kp = (e & 3) + 4 * ((e >> 3) & 3);
+      const int tb = ((e >> 2) & 1) + 2 * ((e >> 5) & 1);
+      const int q = e >> 6;
+      const int nl = q / g.gc, cl = q - nl * g.gc;
+      yt0[i] = 4 * tb;
+      yld[i] = (g.hbytes >> 2) + cl * (g.ystride >> 2) + (nl * T + 4 * tb) * T2_YROW + 4 * kp;
+      yst0[i] = t2_off(2 + (q >> 1), 2 * kp, 32 * (q & 1) + 8 * tb);
+      yst1[i] = yst0[i] + 128 + (((yst0[i] >> 4) & 1) ? -16 : 16);
+    }
     int s = 0;
     uint32_t ph = 0;
     for (int gl = 0; gl < ngroups; ++gl) {
       for (int j = 0; j < nch; ++j) {
-        mbar_wait(&raw_full[s], ph);
+        T2_WAIT(&raw_full[s], ph, 1);
         char* st = smem + L.stg + s * g.stage_bytes;
-        const float* hraw = reinterpret_cast<const float*>(st);
-        const float* yraw = reinterpret_cast<const float*>(st + g.hbytes);
-        // H task e: quad jq of antenna row k (+4 r) of unit q; 16-lane phases
-        // = 8 quads x rows {k, k + 4} (conflict-free loads and 8-byte stores)
+        if (T2_ABLATE(4)) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv_full[s]);
+          if (++s == NS) {
+            s = 0;
+            ph ^= 1u;
+          }
+          continue;
+        }
+        const float* sf = reinterpret_cast<const float*>(st);
         float4 hv[HT];
-        int hoff[HT];
 #pragma unroll
-        for (int i = 0; i < HT; ++i) {
-          const int e = ct + i * T2_CT;
-          int jq, r, kk, q;
-          if (qpr == 8) {
-            jq = e & 7;
-            r = (e >> 3) & 1;
-            kk = (e >> 4) & 15;
-            q = e >> 8;
-          } else {
-            jq = e % qpr;
-            const int e2 = e / qpr;
-            r = e2 & 1;
-            kk = (e2 >> 1) & 15;
-            q = e2 >> 5;
-          }
-          const int k = (kk & 3) + 8 * (kk >> 2) + 4 * r;
-          hoff[i] = -1;
-          hv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (e < nh) {
-            hv[i] = *reinterpret_cast<const float4*>(hraw + (q * 32 + k) * 2 * us + 4 * jq);
-            hoff[i] = t2_off(q >> 1, k, 32 * (q & 1) + 4 * jq);
-          }
-        }
-        // Y task e: antenna pair kp, symbol block tb (t = 4 tb .. 4 tb + 3) of
-        // unit q; 8-lane phases = 4 antenna pairs x 2 symbol blocks
+        for (int i = 0; i < HT; ++i)
+          hv[i] = (hst[i] >= 0) ? *reinterpret_cast<const float4*>(sf + hld[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 yv[YT][4];
-        int yoff[YT];
 #pragma unroll
-        for (int i = 0; i < YT; ++i) {
-          const int e = ct + i * T2_CT;
-          const int kp = (e & 3) + 4 * ((e >> 3) & 3);
-          const int tb = ((e >> 2) & 1) + 2 * ((e >> 5) & 1);
-          const int q = e >> 6;
-          const int nl = q / g.gc, cl = q - nl * g.gc;
-          const float* yq = yraw + cl * (g.ystride >> 2) + nl * T * T2_YROW;
+        for (int i = 0; i < YT; ++i)
 #pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int t = 4 * tb + x;
-            yv[i][x] = (t < T) ? *reinterpret_cast<const float4*>(yq + t * T2_YROW + 4 * kp)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          yoff[i] = t2_off(2 + (q >> 1), 2 * kp, 32 * (q & 1) + 8 * tb);
-        }
+          for (int x = 0; x < 4; ++x)
+            yv[i][x] = (yt0[i] + x < T) ? *reinterpret_cast<const float4*>(sf + yld[i] + x * T2_YROW)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
         named_bar(1, T2_CT);  // every load of the stage done: convert in place
 #pragma unroll
         for (int i = 0; i < HT; ++i) {
-          if (hoff[i] < 0) continue;
+          if (hst[i] < 0) continue;
           uint32_t w0[NSPLIT], w1[NSPLIT];
           split2<NSPLIT>(hv[i].x, hv[i].y, w0);
           split2<NSPLIT>(hv[i].z, hv[i].w, w1);
 #pragma unroll
           for (int sp = 0; sp < NSPLIT; ++sp)
-            *reinterpret_cast<uint2*>(st + sp * T2_SPLIT_BYTES + hoff[i]) = make_uint2(w0[sp], w1[sp]);
+            *reinterpret_cast<uint2*>(st + sp * T2_SPLIT_BYTES + hst[i]) = make_uint2(w0[sp], w1[sp]);
         }
 #pragma unroll
         for (int i = 0; i < YT; ++i) {
@@ -397,14 +675,10 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
           split2<NSPLIT>(yv[i][1].z, yv[i][1].w, b1);
           split2<NSPLIT>(yv[i][2].z, yv[i][2].w, b2);
           split2<NSPLIT>(yv[i][3].z, yv[i][3].w, b3);
-          // row 2kp + 1 sits at the next 128-byte K row; its chunk position is
-          // the XOR with (k % 8) flipped in bit 0
-          const int o0 = yoff[i];
-          const int o1 = o0 + 128 + (((o0 >> 4) & 1) ? -16 : 16);
 #pragma unroll
           for (int sp = 0; sp < NSPLIT; ++sp) {
-            *reinterpret_cast<uint4*>(st + sp * T2_SPLIT_BYTES + o0) = make_uint4(a0[sp], a1[sp], a2[sp], a3[sp]);
-            *reinterpret_cast<uint4*>(st + sp * T2_SPLIT_BYTES + o1) = make_uint4(b0[sp], b1[sp], b2[sp], b3[sp]);
+            *reinterpret_cast<uint4*>(st + sp * T2_SPLIT_BYTES + yst0[i]) = make_uint4(a0[sp], a1[sp], a2[sp], a3[sp]);
+            *reinterpret_cast<uint4*>(st + sp * T2_SPLIT_BYTES + yst1[i]) = make_uint4(b0[sp], b1[sp], b2[sp], b3[sp]);
           }
         }
         fence_proxy_async_smem();
@@ -419,92 +693,134 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
   } else {
     // ----------------------------------------------------------- solvers ----
     const int sv = warp - T2_FIRST_SOLV;
-    const int sset = sv >> 2;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int sset = sv >> 2;  // = the accumulator this warp reads
+    const int q = warp & 3;    // TMEM lane quarter this warp may access
     const Team<32, -1> tm{lane};
-    Work w;
-    {
+    Work w[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
       WorkLayout wl = L.w;
-      const int base = L.work + sv * L.work_stride;
+      const int base = L.work + (2 * sv + k) * L.work_stride;
       wl.G += base; wl.Z += base; wl.X += base; wl.W += base; wl.Sv += base; wl.Vv += base; wl.Fb += base;
       wl.gb += base; wl.num += base; wl.phi += base; wl.coef += base; wl.s2 += base; wl.gn += base;
       wl.dg += base; wl.den += base; wl.harm += base; wl.wbuf += base; wl.flags += base;
-      w = make_work(smem, wl, 16);
+      w[k] = make_work(smem, wl, 16);
     }
-    const int u = p.u, T = p.T, LD = w.LD;
+    const int u = p.u, T = p.T, LD = w[0].LD;
     const int uh = lane >> 1, s_im = lane & 1;  // this lane's H feature: UE uh, re/im
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
     int cl_first = 1;
-    for (int gl = sset; gl < ngroups; gl += T2_NSET) {
-      const int a = gl & 1;
-      const int64_t uid = (g_first + gl) * 4 + q;
-      const bool valid = uid < g.U_tot;
-      const int64_t n = uid / g.upi;
-      const int c = (int)(uid - n * g.upi);
-      const float n0 = (valid && MODE != T2_STATS) ? item_n0(p, n) : 0.f;  // global load before the wait
-      mbar_wait(&acc_full[a], (uint32_t)((gl >> 1) & 1));
-      tc_fence_after();
-      uint32_t gr[32], yr[32];
-      tmem_ld32_nw(tq + (uint32_t)(256 * a + 32 * q), gr);
-      tmem_ld32_nw(tq + (uint32_t)(256 * a + 128 + 32 * q), yr);
-      tmem_ld_wait();
-      tc_fence_before();
+    for (int gl = sset; gl < ngroups; gl += 4) {
+      int64_t n[2];
+      int c[2];
+      float n0[2];
+      bool valid[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {  // groups gl, gl + 2 (accumulator sset)
+        valid[k] = false;
+        n[k] = 0;
+        c[k] = 0;
+        n0[k] = 0.f;
+        const int gg = gl + 2 * k;
+        if (gg >= ngroups) continue;
+        const int64_t uid = (g_first + gg) * 4 + q;
+        valid[k] = uid < g.U_tot;
+        n[k] = uid / g.upi;
+        c[k] = (int)(uid - n[k] * g.upi);
+        if (valid[k] && MODE != T2_STATS) n0[k] = item_n0(p, n[k]);  // global load before the wait
+        T2_WAIT(&acc_full[sset], (uint32_t)((gg >> 1) & 1), 1);
+        tc_fence_after();
+        uint32_t gr[32], yr[32];
+        tmem_ld32_nw(tq + (uint32_t)(256 * sset + 32 * q), gr);
+        tmem_ld32_nw(tq + (uint32_t)(256 * sset + 128 + 32 * q), yr);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[sset]);
+        if (T2_ABLATE(1)) valid[k] = false;
+        if (!valid[k]) continue;
+        // re/im recombination (one shuffle per column pair): even lanes form
+        // the real parts, odd lanes the imaginary parts
+        float* Gf = reinterpret_cast<float*>(w[k].G);
+        float* Zf = reinterpret_cast<float*>(w[k].Z);
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float mine = __uint_as_float(gr[2 * v]);
+          const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(gr[2 * v + 1]), 1);
+          const float val = s_im ? (po - mine) : (mine + po);
+          if (uh < u && v < u) Gf[(uh * LD + v) * 2 + s_im] = val;
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const float mine = __uint_as_float(yr[2 * t]);
+          const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(yr[2 * t + 1]), 1);
+          const float val = s_im ? (po - mine) : (mine + po);
+          if (t < T) Zf[(t * LD + uh) * 2 + s_im] = (uh < u) ? val : 0.f;  // zero past u: read by t2_solve_pair
+        }
+        reset_flags(w[k], tm);
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[a]);
-      if (!valid) continue;
-      // re/im recombination (one shuffle per column pair): even lanes form
-      // the real parts, odd lanes the imaginary parts
-      float* Gf = reinterpret_cast<float*>(w.G);
-      float* Zf = reinterpret_cast<float*>(w.Z);
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const float mine = __uint_as_float(gr[2 * v]), po = __shfl_xor_sync(0xffffffffu, __uint_as_float(gr[2 * v + 1]), 1);
-        const float val = s_im ? (po - mine) : (mine + po);
-        if (uh < u && v < u) Gf[(uh * LD + v) * 2 + s_im] = val;
-      }
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const float mine = __uint_as_float(yr[2 * t]), po = __shfl_xor_sync(0xffffffffu, __uint_as_float(yr[2 * t + 1]), 1);
-        const float val = s_im ? (po - mine) : (mine + po);
-        if (uh < u && t < T) Zf[(t * LD + uh) * 2 + s_im] = val;
-      }
-      reset_flags(w, tm);
-      tm.sync();
+      if (!valid[0] && !valid[1]) continue;
       if constexpr (MODE == T2_STATS) {
-        unit_epilogue<16, Team<32, -1>, 0>(w, p, n, c, true, cl_first, tm, nullptr, n0);
-      } else if constexpr (MODE == T2_PD) {
-        unit_epilogue<16, Team<32, -1>, 1>(w, p, n, 0, true, cl_first, tm, nullptr, n0);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (valid[k]) unit_epilogue<16, Team<32, -1>, 0>(w[k], p, n[k], c[k], true, cl_first, tm, nullptr, 0.f);
+        continue;
+      }
+      if constexpr (mrc) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!valid[k]) continue;
+          if constexpr (MODE == T2_PD_MRC) {
+            unit_epilogue<16, Team<32, -1>, 1>(w[k], p, n[k], 0, true, cl_first, tm, nullptr, n0[k]);
+          } else {
+            EpiArgs ea;
+            ea.kind = p.kind;
+            ea.u = u;
+            ea.T = T;
+            ea.n0 = n0[k];
+            ea.es = p.es;
+            ea.damping = p.damping;
+            ea.t_max = p.t_max;
+            ea.beta = p.cl_beta[c[k]];
+            ea.lama_scale = p.cl_scale[c[k]];
+            ea.unbias = true;
+            ea.ablate = 0;
+            linear_unit<16>(w[k], ea, tm);
+            fd_stash(w[k], p, n[k], c[k], tm);
+          }
+        }
       } else {
-        EpiArgs ea;
-        ea.kind = p.kind;
-        ea.u = u;
-        ea.T = T;
-        ea.n0 = n0;
-        ea.es = p.es;
-        ea.damping = p.damping;
-        ea.t_max = p.t_max;
-        ea.beta = p.cl_beta[c];
-        ea.lama_scale = p.cl_scale[c];
-        ea.unbias = true;  // fusion.py:148 -- fuse in the unbiased domain
-        ea.ablate = 0;
-        linear_unit<16>(w, ea, tm);
-        // stash this cluster's estimate, count the arrival; the last of the
-        // item's C clusters folds the records in cluster order
-        fd_stash(w, p, n, c, tm);
-        __threadfence_block();
-        tm.sync();
-        int last = 0;
-        if (lane == 0) last = (atomicAdd(&fd_count[n & (T2_FD_CNT - 1)], 1) == p.C - 1);
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          if (lane == 0) fd_count[n & (T2_FD_CNT - 1)] = 0;
+        t2_solve_pair<MODE == T2_FD>(w, p, n, c, n0, valid, lane);
+      }
+      if constexpr (fd) {
+        // count the arrivals; the last of an item's C clusters folds the
+        // records in cluster order (fusion.py:141-154); Z is free scratch now
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!valid[k]) continue;
           __threadfence_block();
-          fd_finish(reinterpret_cast<float*>(w.X), p, n, tm);
+          __syncwarp();
+          int last = 0;
+          if (lane == 0) last = (atomicAdd(&fd_count[n[k] & (T2_FD_CNT - 1)], 1) == p.C - 1);
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) {
+            if (lane == 0) fd_count[n[k] & (T2_FD_CNT - 1)] = 0;
+            __threadfence_block();
+            fd_finish(reinterpret_cast<float*>(w[k].Z), p, n[k], tm);
+          }
         }
       }
-      tm.sync();
+      __syncwarp();
     }
   }
+#ifdef DBP_STUDY
+  if (p.dbg && lane == 0) {
+    dbgc[0] = clock64() - t_start;
+    for (int k = 0; k < 4; ++k)
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg + warp * 4 + k), (unsigned long long)dbgc[k]);
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
