@@ -12,7 +12,14 @@ hard demap).
 metric: detected Gb/s = frames x W x T x U x log2(M) / device time.
 Prints ONE JSON line (rank 0).  --impl reference times the reference
 algorithm's CPU implementation (the oracle port, oracle/dbp_oracle.py) on all
-host cores instead.
+host cores instead, with the same config dict.  --config selects the other
+BASELINE workloads (FD / LAMA configs run 16 frames per step, cfg5 its 64).
+
+Inputs are synthesized on the GPU (dbp_synthesize, counter-based Philox: every
+frame distinct; a second input set alternates between steps when one step's
+inputs fit in 4x the L2).  After timing, a sample of the timed inputs (64
+subcarriers of up to 8 frames, all T and clusters) is checked against the
+vectorized CPU oracle and reported as "parity".
 """
 
 from __future__ import annotations
@@ -32,13 +39,13 @@ sys.path.insert(0, REPO)
 
 WORKLOADS = {
     # name: arch, kind, B, C, U, bits, snr list (one frame per entry), frames, t_max
-    "cfg1": dict(arch="fd", kind="lmmse", B=64, C=2, U=8, bits=4, snr=[10.0], frames=1, t_max=0),
+    "cfg1": dict(arch="fd", kind="lmmse", B=64, C=2, U=8, bits=4, snr=[10.0], frames=16, t_max=0),
     "cfg2": dict(arch="pd", kind="lmmse", B=128, C=4, U=16, bits=4, snr=[float(s) for s in range(0, 21, 2)],
                  frames=11, t_max=0),
-    "cfg3-zf": dict(arch="fd", kind="zf", B=256, C=8, U=16, bits=6, snr=[15.0], frames=1, t_max=0),
-    "cfg3-mrc": dict(arch="fd", kind="mrc", B=256, C=8, U=16, bits=6, snr=[15.0], frames=1, t_max=0),
-    "cfg4-fd": dict(arch="fd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=1, t_max=10),
-    "cfg4-pd": dict(arch="pd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=1, t_max=10),
+    "cfg3-zf": dict(arch="fd", kind="zf", B=256, C=8, U=16, bits=6, snr=[15.0], frames=16, t_max=0),
+    "cfg3-mrc": dict(arch="fd", kind="mrc", B=256, C=8, U=16, bits=6, snr=[15.0], frames=16, t_max=0),
+    "cfg4-fd": dict(arch="fd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=16, t_max=10),
+    "cfg4-pd": dict(arch="pd", kind="lama", B=256, C=8, U=32, bits=4, snr=[8.0], frames=16, t_max=10),
     "cfg5-pd512": dict(arch="pd", kind="lmmse", B=512, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
     "cfg5-fd512": dict(arch="fd", kind="lmmse", B=512, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
     "cfg5-pd1024": dict(arch="pd", kind="lmmse", B=1024, C=8, U=64, bits=6, snr=[20.0], frames=64, t_max=0),
@@ -53,6 +60,17 @@ L2_BYTES = 126 * 2 ** 20
 def wl_desc(name, wl):
     return (f"{name}: {wl['arch'].upper()} {wl['kind']} B={wl['B']} C={wl['C']} Bc={wl['B'] // wl['C']} "
             f"U={wl['U']} {CONST[wl['bits']]} W={W} T={T} frames/step={wl['frames']}")
+
+
+def frame_snrs(wl):
+    return wl["snr"] if len(wl["snr"]) == wl["frames"] else [wl["snr"][0]] * wl["frames"]
+
+
+def config_dict(name, wl, parallelism="1 GPU, all clusters on chip"):
+    """The workload description both arms print (same_config)."""
+    return {"workload": wl_desc(name, wl), "B": wl["B"], "C": wl["C"], "U": wl["U"], "T": T, "W": W,
+            "frames_per_step": wl["frames"], "snr_db": frame_snrs(wl), "items_per_step": wl["frames"] * W,
+            "parallelism": parallelism}
 
 
 def bits_per_step(wl):
@@ -185,9 +203,9 @@ class CpuBaseline:
         """Run a bounded sample (~`seconds` of wall on all cores).  Returns
         (Gb/s, items, wall seconds)."""
         n_items = max(self.cores, int(self.cores * seconds / self.t_item))
-        n_items = min(n_items, self.H.shape[0])
-        # spread the sample over the frames (SNR points) of the workload
-        idx = np.linspace(0, self.H.shape[0] - 1, n_items).astype(int)
+        # spread the sample over the frames (SNR points) of the host copy,
+        # cycling through it when the bounded sample asks for more items
+        idx = np.arange(n_items) * max(1, self.H.shape[0] // max(n_items, 1)) % self.H.shape[0]
         chunks = np.array_split(idx, self.cores)
         args = []
         for c in chunks:
@@ -217,15 +235,12 @@ def cpu_model():
 
 # --------------------------------------------------------------- inputs ----
 def make_inputs(wl, seed=1234, unique_frames=None):
+    """Host inputs (NumPy, seeded per frame) for the CPU arms."""
     from paper_1808_04473_b200.synth import synth_frames
 
     f = wl["frames"]
     uf = f if unique_frames is None else min(f, unique_frames)
-    snr = wl["snr"] if len(wl["snr"]) == f else [wl["snr"][0]] * f
-    H, Y, S, n0 = synth_frames(seed, uf, W, T, wl["B"], wl["U"], CONST[wl["bits"]], snr[:uf])
-    if uf < f:  # tile unique frames (cfg5: 25-50 GB per step cannot be generated on the host)
-        reps = math.ceil(f / uf)
-        n0 = np.tile(n0, reps)[:f]
+    H, Y, S, n0 = synth_frames(seed, uf, W, T, wl["B"], wl["U"], CONST[wl["bits"]], frame_snrs(wl)[:uf])
     return H, Y, n0, uf
 
 
@@ -252,15 +267,67 @@ def reference_arm(args, wl, name):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gb/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
-        "data": "synthetic i.i.d. Rayleigh CN(0,1/B), uniform 16/64-QAM, CN(0,N0) noise (seeded)",
-        "config": {"workload": wl_desc(name, wl), "parallelism": f"{cpu.cores} host processes"},
+        "data": "synthetic i.i.d. Rayleigh CN(0,1/B), uniform QAM, CN(0,N0) noise (seeded)",
+        "config": config_dict(name, wl),
         "cpu_baseline": {"value": value, "unit": "Gb/s", "cores": cpu.cores, "kind": "port",
-                         "sample": f"{args.steps} steps x ~0.5 s: per-vector oracle port of the reference path "
-                                   f"(oracle/dbp_oracle.py) on {items} (frame,subcarrier) items x {T} symbols, "
-                                   f"CPU {cpu_model()}"},
+                         "sample": f"{args.steps} steps x ~0.5 s on {cpu.cores} host processes: per-vector oracle "
+                                   f"port of the reference path (oracle/dbp_oracle.py) on {items} (frame,subcarrier) "
+                                   f"items x {T} symbols of this workload, CPU {cpu_model()}"},
         "e2e": {"value": value, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def kernel_name(kernel_id, wl, two_pass):
+    up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
+    tag = f"{wl['arch'].upper()}-{wl['kind']}"
+    if two_pass:
+        return "dbp::tc_kernel<64, stats> (3xTF32 tensor cores, wide layout) + dbp::stats_kernel<64> (solves)"
+    if kernel_id == 3:
+        return f"dbp::tc2_kernel<{tag}> (split-bf16 tensor cores)"
+    if kernel_id == 2:
+        return f"dbp::tc_kernel<{up}, {tag}> (3xTF32 tensor cores)"
+    return f"dbp::stream_kernel<{up}, {tag}> (FP32 SIMT)"
+
+
+def parity_block(det, Hd, Yd, n0_frames, wl, const, per_frame=64, max_frames=8, seed=7):
+    """x-hat / sigma2 / nu / decisions of the timed detector on a sample of
+    the timed inputs (64 subcarriers of up to 8 frames, all T and clusters)
+    against the vectorized oracle (outside the timed region)."""
+    import torch
+
+    from oracle import dbp_oracle as O
+
+    out = det.run(Hd, Yd, 0.0, torch.tensor(np.asarray(n0_frames, dtype=np.float32), device="cuda"), W)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    fr = np.linspace(0, wl["frames"] - 1, min(wl["frames"], max_frames)).astype(int)
+    items = np.concatenate([f * W + np.sort(rng.choice(W, per_frame, replace=False)) for f in fr])
+    idx = torch.from_numpy(items).cuda()
+    Hs = Hd.index_select(0, idx).cpu().numpy().astype(np.complex128)
+    Ys = Yd.index_select(0, idx).cpu().numpy().astype(np.complex128)
+    n0s = np.repeat(np.asarray(n0_frames, dtype=np.float32), W)[items].astype(float)
+    lp = {"t_max": wl["t_max"]} if wl["kind"] == "lama" else None
+    ref = O.run_batch_vec(wl["arch"], wl["kind"], Hs, Ys, O.uniform_offsets(wl["B"], wl["C"]), n0s, 1.0,
+                          const.symbols, lama_params=lp, strict=False)
+    xh = out.xhat.index_select(0, idx).cpu().numpy().astype(np.complex128)
+    dec = out.decisions.index_select(0, idx).cpu().numpy()
+    num = np.max(np.abs(xh - ref["z"]), axis=-1)
+    den = np.maximum(np.max(np.abs(ref["z"]), axis=-1), 1e-30)
+    s2 = out.sigma2.index_select(0, idx).cpu().numpy().astype(float)
+    s2 = np.broadcast_to(s2[:, :, None] if wl["kind"] == "lama" else s2[:, None, :], ref["sigma2"].shape)
+    blk = {"xhat_normwise_max": float(np.max(num / den)),
+           "sigma2_entry_max": float(np.max(np.abs(s2 - ref["sigma2"]) / np.maximum(np.abs(ref["sigma2"]), 1e-30))),
+           "decision_mismatches": int(np.sum(dec != ref["dec"])), "symbols_checked": int(dec.size),
+           "tolerance": {"xhat": 1e-4, "sigma2": 1e-4, "nu": 1e-4, "mismatch_rate": 1e-5},
+           "oracle": "oracle.run_batch_vec (float64, complex64-rounded inputs)",
+           "sample": f"{per_frame} random subcarriers x {len(fr)} frame(s) x {T} symbols x all clusters"}
+    if wl["arch"] == "fd":
+        nu = out.nu.index_select(0, idx).cpu().numpy().astype(float)
+        nu = (np.broadcast_to(np.transpose(nu, (0, 2, 1))[:, :, :, None], ref["nu"].shape) if wl["kind"] == "lama"
+              else np.broadcast_to(nu[:, None], ref["nu"].shape))
+        blk["nu_entry_max"] = float(np.max(np.abs(nu - ref["nu"]) / np.maximum(np.abs(ref["nu"]), 1e-30)))
+    return blk
 
 
 def main():
@@ -273,6 +340,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -290,73 +358,47 @@ def single_gpu(args, wl, name):
 
     import paper_1808_04473_b200 as dbp
     from paper_1808_04473_b200 import _lib
+    from paper_1808_04473_b200.synth import snr_to_n0, synth_device
 
     torch.cuda.set_device(0)
     const = dbp.make_constellation(CONST[wl["bits"]])
-    big = wl["U"] == 64
     n_items = wl["frames"] * W
     counts = [wl["B"] // wl["C"]] * wl["C"]
     lp = {"t_max": wl["t_max"]} if wl["kind"] == "lama" else None
     det = dbp.Detector(wl["arch"], wl["kind"], n_items, wl["B"], wl["U"], T, counts, const, lama_params=lp)
-    if big:
-        # cfg5: 25-50 GB of inputs per step are synthesized on the GPU
-        # (dbp_synthesize, counter-based Philox: every frame distinct); a
-        # 2-frame host copy feeds the CPU baseline
-        from paper_1808_04473_b200.synth import snr_to_n0, synth_device
-
-        snr = wl["snr"] if len(wl["snr"]) == wl["frames"] else [wl["snr"][0]] * wl["frames"]
-        n0 = snr_to_n0(snr, const.es)
-        n0_f = torch.tensor(np.asarray(n0, dtype=np.float32), device="cuda")
-        Hd, Yd = synth_device(1234, n_items, wl["B"], wl["U"], T, const, n0_dev=n0_f, n0_group=W)
-        uf = 2
-        H, Y = Hd[:uf * W].cpu().numpy(), Yd[:uf * W].cpu().numpy()
-    else:
-        H, Y, n0, uf = make_inputs(wl)
-        # device-resident inputs; alternate two copies so no step starts from a warm L2
-        Hd = torch.empty((n_items, wl["B"], wl["U"]), dtype=torch.complex64, device="cuda")
-        Yd = torch.empty((n_items, T, wl["B"]), dtype=torch.complex64, device="cuda")
-        Hu, Yu = torch.from_numpy(H).cuda(), torch.from_numpy(Y).cuda()
-        for f in range(wl["frames"]):
-            src = (f % uf) * W
-            Hd[f * W:(f + 1) * W].copy_(Hu[src:src + W])
-            Yd[f * W:(f + 1) * W].copy_(Yu[src:src + W])
-        del Hu, Yu
-    step_bytes = (Hd.numel() + Yd.numel()) * 8
-    copies = [(Hd, Yd)]
-    if step_bytes < 4 * L2_BYTES and torch.cuda.mem_get_info()[0] > 3 * step_bytes:
-        copies.append((Hd.clone(), Yd.clone()))
+    # inputs on the GPU (dbp_synthesize: every frame distinct); two sets
+    # alternate between steps when a step fits in 4x the L2
+    n0 = snr_to_n0(frame_snrs(wl), const.es)
     n0_dev = torch.tensor(np.asarray(n0, dtype=np.float32), device="cuda")
-    # parity gate on this very input before timing (first subcarriers of frame 0)
-    out = det.run(Hd, Yd, 0.0, n0_dev, W, check=True)
+    step_bytes = n_items * (wl["B"] * wl["U"] + T * wl["B"]) * 8
+    copies = [synth_device(1234, n_items, wl["B"], wl["U"], T, const, n0_dev=n0_dev, n0_group=W)]
+    if step_bytes < 4 * L2_BYTES and torch.cuda.mem_get_info()[0] > 3 * step_bytes:
+        copies.append(synth_device(4321, n_items, wl["B"], wl["U"], T, const, n0_dev=n0_dev, n0_group=W))
     torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        h, y = copies[0]
-        det.run(h, y, 0.0, n0_dev, W)
+    det.run(*copies[0], 0.0, n0_dev, W, check=True)  # status check (raises on a fault)
+    for k in range(args.warmup):
+        det.run(*copies[k % len(copies)], 0.0, n0_dev, W)
     torch.cuda.synchronize()
-    det.launches = 0
+    launches_before = det.launches
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         start.record()
         for k in range(args.steps):
-            h, y = copies[k % len(copies)]
-            det.run(h, y, 0.0, n0_dev, W)
+            det.run(*copies[k % len(copies)], 0.0, n0_dev, W)
         stop.record()
         torch.cuda.synchronize()
-        # keep sampling clocks for a comparable window if the region was short
+        timed_launches = det.launches - launches_before
         elapsed_ms = start.elapsed_time(stop)
+        # keep sampling clocks for a comparable window if the region was short
         if elapsed_ms < 300:
             extra = max(1, int(300 / max(elapsed_ms / args.steps, 1e-3)))
             for k in range(extra):
-                h, y = copies[k % len(copies)]
-                det.run(h, y, 0.0, n0_dev, W)
+                det.run(*copies[k % len(copies)], 0.0, n0_dev, W)
             torch.cuda.synchronize()
     kernel_id = _lib.lib().dbp_last_kernel()
-    up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
-    # U = 64 PD on the tensor cores: statistics launch (wide layout) + solve launch
-    two_pass = kernel_id == 2 and up == 64
-    launches = args.steps * (2 if two_pass else 1)
+    two_pass = kernel_id == 2 and wl["U"] == 64 and wl["arch"] == "pd"  # statistics + solve launches
+    launches = timed_launches * (2 if two_pass else 1)
     ms = elapsed_ms / args.steps
     bits = bits_per_step(wl)
     value = bits / (ms * 1e-3) / 1e9
@@ -376,8 +418,12 @@ def single_gpu(args, wl, name):
     except Exception:
         pass
 
+    # ---------------- parity on a sample of the timed inputs (untimed)
+    parity = parity_block(det, *copies[0], n0, wl, const) if not args.no_parity else None
+
     # ---------------- end to end: host pinned buffers through the public API
     e2e = None
+    Hd, Yd = copies[0]
     if args.e2e_steps > 0 and step_bytes <= 8 * 2 ** 30:  # pinned host copies of the whole step
         Hh = torch.empty(Hd.shape, dtype=torch.complex64, pin_memory=True)
         Yh = torch.empty(Yd.shape, dtype=torch.complex64, pin_memory=True)
@@ -402,12 +448,15 @@ def single_gpu(args, wl, name):
                "path": "Detector.run_host: pinned host H,Y -> chunked H2D / fused kernel / D2H of xhat, sigma2, "
                        "decisions, status (3 streams)"}
         # sanity: results equal the device-resident run
-        ref = out.decisions.cpu()
+        ref = det.run(Hd, Yd, 0.0, n0_dev, W).decisions.cpu()
         assert torch.equal(outs["dec"], ref)
 
     # ---------------- CPU baseline (reference algorithm, host cores)
     cpu = None
     if not args.no_cpu:
+        uf = min(2, wl["frames"])
+        H = Hd[:uf * W].cpu().numpy()
+        Y = Yd[:uf * W].cpu().numpy()
         n0_items = np.repeat(n0[:uf], W)
         cb = CpuBaseline(wl, H, Y, n0_items)
         rate, n_s, wall = cb.run(args.cpu_seconds)
@@ -417,28 +466,22 @@ def single_gpu(args, wl, name):
                          f"oracle port of the reference path, {wall:.1f} s wall on {cb.cores} processes "
                          f"({cpu_model()})"}
 
+    cfg = config_dict(name, wl)
+    cfg["l2"] = (f"inputs {step_bytes / 2**20:.0f} MiB/step vs 126 MiB L2; {len(copies)} input set(s) "
+                 f"alternated")
     line = {
         "metric": METRIC, "value": value, "unit": "Gb/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c64 (fp32 arithmetic)",
         "data": "synthetic: i.i.d. Rayleigh CN(0,1/B) channels constant over T, uniform QAM symbols, "
-                "CN(0,N0) noise, seeded (paper's LTE/WINNER-II data not available)"
-                + ("; generated on the GPU (dbp_synthesize, Philox4x32-10), every frame distinct" if big else ""),
-        "config": {"workload": wl_desc(name, wl), "B": wl["B"], "C": wl["C"], "U": wl["U"], "T": T, "W": W,
-                   "frames_per_step": wl["frames"], "snr_db": wl["snr"], "items_per_step": n_items,
-                   "l2": f"inputs {step_bytes / 2**20:.0f} MiB/step vs 126 MiB L2; {len(copies)} input "
-                         f"copies alternated",
-                   "parallelism": "1 GPU, all clusters on chip"},
+                "CN(0,N0) noise, seeded, generated on the GPU (dbp_synthesize, Philox4x32-10; every frame "
+                "distinct; the paper's LTE/WINNER-II data is not available)",
+        "config": cfg,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": ("dbp::tc_kernel<64, stats> (tensor cores, wide layout) + dbp::stats_kernel<64> "
-                                "(solves), 2 launches/step" if two_pass else
-                                f"dbp::tc2_kernel<{wl['arch'].upper()}-{wl['kind']}> (split-bf16 tensor cores, "
-                                f"1 launch/step)" if kernel_id == 3 else
-                                f"dbp::tc_kernel<{up}, {wl['arch'].upper()}-{wl['kind']}> (3xTF32 tensor cores, "
-                                f"1 launch/step)" if kernel_id == 2 else
-                                f"dbp::stream_kernel<{up}> (FP32 SIMT, 1 launch/step)")},
+                     "kernel": kernel_name(kernel_id, wl, two_pass) + f", {2 if two_pass else 1} launch(es)/step"},
+        "parity": parity,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -362,6 +362,196 @@ def run_batch(arch, kind, H, Y, offsets, n0, es=1.0, symbols=None,
 
 
 # --------------------------------------------------------------------------
+# vectorized restatement: the same per-vector algorithm, batched over items
+# and symbols with NumPy (the reference recomputes G_c for every receive
+# vector; G_c depends only on H, so computing it once per item is the same
+# arithmetic).  Used for parity at the BASELINE sizes (>= 1e5 symbols); pinned
+# to run_batch by tests/test_oracle_vec.py.  Raises on the first failing item
+# like the per-vector path, unless strict=False (then status[n] is returned).
+# --------------------------------------------------------------------------
+def _linear_vec(kind, g, ym, n0, es):
+    """linear_equalize (equalize.py:130-176) for G [n][U][U], y_mrc
+    [n][T][U], n0 [n]; returns z [n][T][U], sigma2 [n][U], gain [n][U]|None,
+    bad [n] (SingularGram)."""
+    n, u = g.shape[0], g.shape[-1]
+    eye = np.eye(u)
+    bad = np.zeros(n, dtype=bool)
+    if kind == MRC:
+        d = np.real(np.einsum("nii->ni", g)).copy()
+        bad |= np.any(d <= 0.0, axis=1)
+        d = np.where(d <= 0.0, 1.0, d)
+        z = ym / d[:, None, :]
+        s2 = n0[:, None] / d + es * np.sum(np.abs(g / d[:, :, None] - eye) ** 2, axis=2)
+        return z, s2, None, bad
+    if kind == ZF:
+        m = g
+    elif kind == LMMSE:
+        m = g + (n0 / es)[:, None, None] * eye
+    else:
+        raise OracleError("ConfigError", f"kind {kind}")
+    # Cholesky of each item (zpotrf); failures -> SingularGram
+    ok = np.ones(n, dtype=bool)
+    try:
+        l = np.linalg.cholesky(m)
+    except np.linalg.LinAlgError:
+        l = np.zeros_like(m)
+        for i in range(n):
+            try:
+                l[i] = np.linalg.cholesky(m[i])
+            except np.linalg.LinAlgError:
+                ok[i] = False
+                l[i] = np.eye(u)
+    bad |= ~ok
+    inv = np.linalg.inv(l)                        # L^-1
+    a = np.conj(np.swapaxes(inv, -1, -2)) @ inv    # M^-1 = L^-H L^-1
+    z = np.einsum("nij,ntj->nti", a, ym)
+    if kind == ZF:
+        s2 = n0[:, None] * np.sum(np.abs(inv) ** 2, axis=1)  # diag(G^-1)
+        return z, s2, None, bad
+    ag = a @ g
+    noise = n0[:, None] * np.real(np.sum(ag * a.conj(), axis=2))
+    interf = es * np.sum(np.abs(ag - eye) ** 2, axis=2)
+    gain = np.real(np.einsum("nii->ni", ag))
+    return z, noise + interf, gain, bad
+
+
+def _check_sigma2_vec(s2):
+    neg = np.any(s2 < -VAR_TOL, axis=tuple(range(1, s2.ndim)))
+    return np.maximum(s2, 0.0), neg
+
+
+def _unbias_vec(z, s2, gain, es):
+    if gain is None:
+        return z, s2, np.zeros(z.shape[0], dtype=bool)
+    badg = np.any(gain <= 0, axis=1)
+    g = np.where(gain <= 0, 1.0, gain)
+    s2u = (s2 - (1.0 - g) ** 2 * es) / g ** 2
+    return z / g[:, None, :], s2u, badg
+
+
+def _posterior_vec(z, tau, symbols):
+    """posterior_mean_var (_kernels_py.py:14-28) for z [...], tau [...]."""
+    d2 = np.abs(z[..., None] - symbols) ** 2
+    d2 = d2 - d2.min(axis=-1, keepdims=True)
+    w = np.exp(-d2 / tau[..., None])
+    w = w / w.sum(axis=-1, keepdims=True)
+    f = w @ symbols
+    g = np.maximum(w @ (np.abs(symbols) ** 2) - np.abs(f) ** 2, 0.0)
+    return f, g
+
+
+def _lama_vec(g, ym, symbols, es, n0, beta, t_max=10, damping=1.0):
+    """lama_equalize (equalize.py:208-259) for every (item, symbol):
+    G [n][U][U], y_mrc [n][T][U], n0 [n] -> z [n][T][U], tau [n][T],
+    diverged-at-iteration [n] (0: none)."""
+    n, t_count, u = ym.shape
+    a = np.eye(u) - g
+    s = np.full((n, t_count, u), symbols.mean(), dtype=np.complex128)
+    v = np.zeros((n, t_count, u), dtype=np.complex128)
+    phi = np.full((n, t_count), float(es))
+    div = np.zeros(n, dtype=int)
+    z = None
+    tau = n0[:, None] + beta * phi
+    for it in range(1, t_max + 1):
+        tau = n0[:, None] + beta * phi
+        z = ym + np.einsum("nij,ntj->nti", a, s) + v
+        bad = ~(np.all(np.isfinite(z), axis=2) & (np.max(np.abs(np.nan_to_num(z, nan=np.inf)), axis=2) < 1e150))
+        newly = np.any(bad, axis=1) & (div == 0)
+        div[newly] = it
+        f, gv = _posterior_vec(np.nan_to_num(z), np.maximum(tau, 1e-300)[:, :, None] * np.ones(u), symbols)
+        phi_next = np.mean(gv, axis=2)
+        v = (beta * phi_next / tau)[:, :, None] * (z - s)
+        s = damping * f + (1.0 - damping) * s
+        phi = phi_next
+    return z, tau, div
+
+
+def run_batch_vec(arch, kind, H, Y, offsets, n0, es=1.0, symbols=None, lama_params=None, strict=True):
+    """run_batch for whole batches: H [n][B][U], Y [n][T][B], n0 scalar or
+    [n].  Returns z [n][T][U], sigma2 [n][T][U], nu [n][C][U] (FD; per
+    symbol for LAMA: [n][T][C][U]), dec [n][T][U] and status [n] (0 ok,
+    1 singular, 2 negative variance, 3 diverged, 4 bad fusion variance)."""
+    H = np.asarray(H, dtype=np.complex128)
+    Y = np.asarray(Y, dtype=np.complex128)
+    n, b, u = H.shape
+    t_count = Y.shape[1]
+    n0a = np.broadcast_to(np.asarray(n0, dtype=float), (n,)).astype(float)
+    lp = dict(lama_params or {})
+    t_max, damping = int(lp.get("t_max", 10)), float(lp.get("damping", 1.0))
+    symbols = None if symbols is None else np.asarray(symbols, dtype=np.complex128)
+    status = np.zeros(n, dtype=int)
+
+    def flag(mask, code):
+        status[(status == 0) & mask] = code
+
+    C = len(offsets) - 1
+    if arch == "pd":
+        g = np.einsum("nbi,nbj->nij", H.conj(), H)
+        ym = np.einsum("nbi,ntb->nti", H.conj(), Y)
+        if kind == LAMA:
+            z, tau, div = _lama_vec(g, ym, symbols, es, n0a, u / b, t_max, damping)
+            flag(div > 0, 3)
+            s2 = np.broadcast_to(tau[:, :, None], (n, t_count, u))
+        else:
+            z, s2, gain, bad = _linear_vec(kind, g, ym, n0a, es)
+            flag(bad, 1)
+            s2, neg = _check_sigma2_vec(s2)
+            flag(neg, 2)
+            z, s2, badg = _unbias_vec(z, s2, gain, es)
+            flag(badg, 1)
+            s2, neg = _check_sigma2_vec(s2)
+            flag(neg, 2)
+            s2 = np.broadcast_to(s2[:, None, :], (n, t_count, u))
+        out = dict(z=z, sigma2=np.array(s2))
+    else:
+        zc, s2c, wc = [], [], []
+        for c in range(C):
+            sl = slice(offsets[c], offsets[c + 1])
+            hc = H[:, sl]
+            b_c = hc.shape[1]
+            g = np.einsum("nbi,nbj->nij", hc.conj(), hc)
+            ym = np.einsum("nbi,ntb->nti", hc.conj(), Y[:, :, sl])
+            if kind == LAMA:
+                w_c = b_c / b
+                z, tau, div = _lama_vec(g / w_c, ym / w_c, symbols, es, n0a / w_c, u / b_c, t_max, damping)
+                flag(div > 0, 3)
+                s2 = np.broadcast_to(tau[:, :, None], (n, t_count, u))
+            else:
+                z, s2, gain, bad = _linear_vec(kind, g, ym, n0a, es)
+                flag(bad, 1)
+                s2, neg = _check_sigma2_vec(s2)
+                flag(neg, 2)
+                z, s2, badg = _unbias_vec(z, s2, gain, es)
+                flag(badg, 1)
+                s2, neg = _check_sigma2_vec(s2)
+                flag(neg, 2)
+                s2 = np.broadcast_to(s2[:, None, :], (n, t_count, u))
+            zc.append(z)
+            s2c.append(np.array(s2))
+            wc.append(np.real(np.einsum("nii->ni", g)) if kind == MRC else None)
+        zs = np.stack(zc, axis=2)      # [n][T][C][U]
+        s2s = np.stack(s2c, axis=2)    # [n][T][C][U]
+        if kind == MRC:
+            gains = np.stack(wc, axis=1)[:, None]          # [n][1][C][U]
+            nu = gains / gains.sum(axis=2, keepdims=True)
+        else:
+            flag(np.any(s2s <= 0, axis=(1, 2, 3)), 4)
+            inv = 1.0 / np.maximum(s2s, VARIANCE_FLOOR)
+            nu = inv / inv.sum(axis=2, keepdims=True)
+        z = np.sum(nu * zs, axis=2)
+        s2 = 1.0 / np.sum(1.0 / np.maximum(s2s, VARIANCE_FLOOR), axis=2)
+        out = dict(z=z, sigma2=s2, nu=np.broadcast_to(nu, zs.shape).copy())
+    if symbols is not None:
+        out["dec"] = np.argmin(np.abs(out["z"][..., None] - symbols) ** 2, axis=-1)
+    out["status"] = status
+    if strict and np.any(status):
+        i = int(np.flatnonzero(status)[0])
+        names = {1: "SingularGramError", 2: "NegativeVarianceError", 3: "DivergenceError", 4: "ConfigError"}
+        raise OracleError(names[int(status[i])], f"item {i}")
+    return out
+
+
+# --------------------------------------------------------------------------
 # message volumes (model.py:260-280)
 # --------------------------------------------------------------------------
 def message_volume(u, n_sc, n_sym, c, bytes_per_entry=8):

@@ -467,6 +467,10 @@ __global__ void __launch_bounds__(TC_MAX_THREADS, 1) tc_kernel(const __grid_cons
             umma_tf32(d, ah, ah, idesc, acc);
             umma_tf32(d, ah, al, idesc, 1u);
             umma_tf32(d, al, ah, idesc, 1u);
+            // U = 64 (B up to 1024 antennas, 64 x 64 solves): the lo.lo term
+            // too (4-term split, ~2^-20 per product instead of ~2^-18), so the
+            // decision-mismatch rate stays below 1e-5 at cfg5 (VERDICT r1 task 5)
+            if constexpr (WIDE) umma_tf32(d, al, al, idesc, 1u);
           }
           if (rec) cnt[3] += clock64() - t_mma;
           first = false;
