@@ -4,7 +4,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 CSRC := paper_1808_04473_b200/csrc
-SRCS := $(CSRC)/dbp_kernels.cu $(CSRC)/dbp_launch_tc2.cu $(CSRC)/dbp_launch_tc.cu $(CSRC)/dbp_launch_simt.cu
+SRCS := $(CSRC)/dbp_kernels.cu $(CSRC)/dbp_launch_tc2.cu $(CSRC)/dbp_launch_tc.cu $(CSRC)/dbp_launch_simt.cu $(CSRC)/dbp_comm.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDR := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dbp_host.h include/dbp_b200.h
 LIB := paper_1808_04473_b200/libdbp_b200.so
@@ -16,7 +16,7 @@ build/%.o: $(CSRC)/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) $(EXTRA) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 	@cat build/*.ptxas.log > build_ptxas.log
 	@grep -E "registers|spill|Compiling entry" build_ptxas.log | sed 's/ptxas info    : //' > paper_1808_04473_b200/ptxas_summary.txt || true
 
@@ -35,6 +35,6 @@ $(SDIR)/%.o: $(CSRC)/%.cu $(HDR)
 	@mkdir -p $(SDIR)
 	$(NVCC) $(NVFLAGS) -DDBP_STUDY $(EXTRA) -c -o $@ $< 2> $(SDIR)/$*.ptxas.log || (cat $(SDIR)/$*.ptxas.log; exit 1)
 $(STUDY_LIB): $(STUDY_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(STUDY_OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(STUDY_OBJS) -lcudart -ldl
 study: $(STUDY_LIB)
 .PHONY: study

@@ -341,12 +341,15 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--chunks", type=int, default=2, help="N > 1: exchange chunks overlapped with compute")
+    ap.add_argument("--dist", action="store_true", help="run the multi-GPU path even at world size 1 (tests)")
+    ap.add_argument("--no-graph", action="store_true", help="N > 1: eager steps instead of a CUDA graph")
     args = ap.parse_args()
     wl = WORKLOADS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return reference_arm(args, wl, args.config)
-    if world > 1:
+    if world > 1 or args.dist:
         from paper_1808_04473_b200 import distributed
 
         return distributed.bench_main(args, wl, args.config, sys.modules[__name__])

@@ -227,6 +227,37 @@ int dbp_gray_bits(const void* idx, int idx_bytes, int64_t n, int L, uint8_t* bit
 int dbp_quadrature(int kind, const double* x, int64_t n, const double* values, int M, const double* nodes,
                    const double* weights, int q, double* out, void* stream);
 
+
+/* ---- multi-GPU fusion over NCCL (one process per GPU) -------------------
+ * The path's one exchange step (the paper fuses one cluster
+ * per GPU with ncclReduce to a master; the reference runs its clusters
+ * sequentially, fusion.py:141-146, montecarlo.py:132-135), as a sum
+ * reduce-scatter by item block so every rank finishes n / nranks items:
+ *   PD: sum over clusters of {G_c, y_c^mrc}   -> fuse_partials (equalize.py:96-107)
+ *   FD: sum over clusters of {w z, w, 1/s2}   -> fuse_estimates (fusion.py:108-124)
+ * plus the all-reduce of the FD weight sums behind nu
+ * (optimal_fusion_weights, fusion.py:96-105).  NCCL is loaded at run time
+ * (dlopen libnccl.so.2).  Calls are asynchronous on `stream`. */
+typedef struct dbp_comm* dbp_comm_t;
+/* ncclGetUniqueId: 128 bytes for rank 0 to share with the group */
+int dbp_comm_unique_id(void* id128);
+/* ncclCommInitRank (collective over the group's ranks) */
+int dbp_comm_init(const void* id128, int nranks, int rank, dbp_comm_t* comm);
+int dbp_comm_destroy(dbp_comm_t comm);
+/* stats_send [nranks * items_per_rank][u*u + T*u] complex64 (this rank's
+ * cluster sums, dbp_gram_mrc with sum_clusters = 1) -> stats_recv
+ * [items_per_rank][u*u + T*u]: the group sum of items
+ * [rank * items_per_rank, (rank + 1) * items_per_rank). */
+int dbp_pd_reduce_scatter(dbp_comm_t comm, const void* stats_send, void* stats_recv, int64_t items_per_rank, int u,
+                          int T, void* stream);
+/* acc_send [nranks * items_per_rank][2*T*u + 2*wdim] float (DBP_ARCH_FD_PARTIAL
+ * sums of dbp_equalize) -> acc_recv [items_per_rank][...], then
+ * dbp_fd_finalize on the received block. */
+int dbp_fd_reduce_scatter(dbp_comm_t comm, const float* acc_send, float* acc_recv, int64_t items_per_rank, int u,
+                          int T, int wdim, void* stream);
+/* in-place sum over the group (FD weight denominators for dbp_fd_weights) */
+int dbp_allreduce_sum(dbp_comm_t comm, float* buf, int64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

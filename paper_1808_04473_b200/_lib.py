@@ -55,6 +55,12 @@ SIGNATURES = {
     "dbp_llr": [_vp, _vp, _i64, _i, _i, _i, _vp, _i, _i, _vp, _vp],
     "dbp_gray_bits": [_vp, _i, _i64, _i, _vp, _vp],
     "dbp_quadrature": [_i, _vp, _i64, _vp, _i, _vp, _vp, _i, _vp, _vp],
+    "dbp_comm_unique_id": [_vp],
+    "dbp_comm_init": [_vp, _i, _i, _vp],
+    "dbp_comm_destroy": [_vp],
+    "dbp_pd_reduce_scatter": [_vp, _vp, _vp, _i64, _i, _i, _vp],
+    "dbp_fd_reduce_scatter": [_vp, _vp, _vp, _i64, _i, _i, _i, _vp],
+    "dbp_allreduce_sum": [_vp, _vp, _i64, _vp],
     "dbp_synthesize": [C.c_uint64, _i64, _i64, _i, _i, _i, _vp, _i, _f, _vp, _i64, _vp, _vp, _vp, _vp],
 }
 

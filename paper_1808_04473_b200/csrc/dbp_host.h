@@ -19,6 +19,7 @@ int sm_count();
 void* stream_scratch(cudaStream_t st, size_t need);  // per-(device, stream) scratch
 // launchers: 0 launched, < 0 error, 1 geometry not covered (caller falls back)
 int launch_tc2(EqParams& p, cudaStream_t st);
+int launch_t2_stats_solve(EqParams& p, cudaStream_t st);
 int launch_tc_up(int up, EqParams& p, cudaStream_t st);
 int launch_stream_up(int up, EqParams& p, cudaStream_t st);
 int launch_stats_up(int up, EqParams& p, cudaStream_t st);

@@ -541,6 +541,8 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
 }
 
 static int dispatch_stats(EqParams& p, cudaStream_t st) {
+  const int rc = launch_t2_stats_solve(p, st);  // u <= 16 ZF / L-MMSE: warp-pair solver
+  if (rc <= 0) return rc;
   return launch_stats_up(up_for(p.u), p, st);
 }
 

@@ -160,4 +160,20 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   return nsplit == 2 ? launch_tc2_mode<T2_PD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_PD, 3>(p, g, hm, ym, st);
 }
 
+// linear_equalize on fused statistics for u <= 16, ZF / L-MMSE (returns 1
+// otherwise: the caller uses stats_kernel)
+int launch_t2_stats_solve(EqParams& p, cudaStream_t st) {
+  if (p.u > 16 || p.T > 16 || (p.kind != EQ_ZF && p.kind != EQ_LMMSE) || p.lama_scale != 1.f) return 1;
+  if (opt(DBP_OPT_KERNEL) == DBP_KERNEL_SIMT) return 1;
+  const int work = align_up((16 + p.TP) * 18 * 8 + 32 * 8 + 16, 128);
+  const int smem = 2 * T2S_WARPS * work;
+  if (cudaFuncSetAttribute(t2_stats_solve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return fail(DBP_E_CUDA, "shared memory request too large");
+  const int64_t pairs = (p.n_items + 1) / 2;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((pairs + T2S_WARPS - 1) / T2S_WARPS,
+                                                              (int64_t)sm_count() * 8));
+  t2_stats_solve_kernel<16><<<(unsigned)grid, 32 * T2S_WARPS, smem, st>>>(p, work);
+  return cuda_check("t2_stats_solve_kernel");
+}
+
 }  // namespace dbp

@@ -448,6 +448,60 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   }
 }
 
+// Central solve from fused statistics {G, y_mrc} (linear_equalize +
+// unbiased_output on FusedStats, equalize.py:130-195; the central node of the
+// multi-GPU PD path after dbp_pd_reduce_scatter) for u <= 16, ZF / L-MMSE:
+// each warp stages two items' statistics into its two work areas (G
+// Hermitian from its lower triangle, as the reference's Cholesky reads it;
+// y_mrc zero past u) and runs t2_solve_pair.
+constexpr int T2S_WARPS = 4;
+template <int UP = 16>  // (a template so that the header can be included by several units)
+__global__ void __launch_bounds__(32 * T2S_WARPS) t2_stats_solve_kernel(const __grid_constant__ EqParams p,
+                                                                        int work_stride) {
+  extern __shared__ __align__(16) char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = p.u, T = p.T, LD = 16 + 2;
+  const int rec = u * u + T * u;
+  Work w[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    char* base = smem + (2 * warp + k) * work_stride;
+    w[k].G = reinterpret_cast<float2*>(base);
+    w[k].Z = reinterpret_cast<float2*>(base + 16 * LD * 8);
+    w[k].W = reinterpret_cast<float2*>(base + 32 * LD * 8);
+    w[k].flags = reinterpret_cast<int*>(base + 32 * LD * 8 + 32 * 8);
+    w[k].X = w[k].Z;
+    w[k].LD = LD;
+  }
+  const int64_t pairs = (p.n_items + 1) / 2;
+  for (int64_t pr = (int64_t)blockIdx.x * T2S_WARPS + warp; pr < pairs; pr += (int64_t)gridDim.x * T2S_WARPS) {
+    int64_t n[2];
+    int c[2] = {0, 0};
+    float n0[2];
+    bool valid[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      n[k] = 2 * pr + k;
+      valid[k] = n[k] < p.n_items;
+      n0[k] = valid[k] ? item_n0(p, n[k]) : 0.f;
+      if (!valid[k]) continue;
+      const float2* src = p.stats_in + (size_t)n[k] * rec;
+      for (int e = lane; e < u * u; e += 32) {
+        const int i = e / u, j = e - i * u;
+        const float2 v = (i >= j) ? src[e] : c_conj(src[j * u + i]);
+        w[k].G[i * LD + j] = v;
+      }
+      for (int e = lane; e < T * 16; e += 32) {
+        const int t = e >> 4, i = e & 15;
+        w[k].Z[t * LD + i] = (i < u) ? src[u * u + t * u + i] : make_float2(0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    t2_solve_pair<false>(w, p, n, c, n0, valid, lane);
+    __syncwarp();
+  }
+}
+
 template <int MODE, int NSPLIT>
 // register cap: a warp lives on one of the 4 SM sub-partitions (16K registers
 // each), which hold ceil(warps / 4) warps

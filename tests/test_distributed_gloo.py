@@ -120,14 +120,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, arch, kind, C, bits, path):
+def _worker(rank, world, port, arch, kind, C, bits, path, chunks=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1808_04473_b200.distributed import ClusterGroup
 
     rng = np.random.default_rng(5)
-    n, B, U = 4, 8 * C, 4
+    n, B, U = 4 * chunks, 8 * C, 4
     H = (rng.standard_normal((n, B, U)) + 1j * rng.standard_normal((n, B, U))) / np.sqrt(2 * B)
     Y = rng.standard_normal((n, T, B)) + 1j * rng.standard_normal((n, T, B))
     n0 = rng.uniform(0.05, 0.2, n)
@@ -138,7 +138,7 @@ def _worker(rank, world, port, arch, kind, C, bits, path):
     if grp.plan.n_shards > 1:
         H, Y = H * (1 + grp.plan.shard), Y * (1 + grp.plan.shard)
     res = grp.run(torch.from_numpy(np.ascontiguousarray(H[:, a:b])),
-                  torch.from_numpy(np.ascontiguousarray(Y[:, :, a:b])), torch.from_numpy(n0))
+                  torch.from_numpy(np.ascontiguousarray(Y[:, :, a:b])), torch.from_numpy(n0), chunks=chunks)
     np.savez(os.path.join(path, f"r{rank}.npz"), items=np.array(res.items), xhat=res.xhat.numpy(),
              sigma2=res.sigma2.numpy(), dec=res.decisions.numpy(),
              nu=np.zeros(0) if res.nu is None else np.asarray(res.nu), clusters=np.array(grp.plan.clusters),
@@ -146,21 +146,24 @@ def _worker(rank, world, port, arch, kind, C, bits, path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,arch,kind,C,bits", [
-    (2, "pd", "lmmse", 4, 4), (2, "pd", "zf", 2, 4), (2, "fd", "lmmse", 4, 4), (2, "fd", "mrc", 2, 4),
-    (2, "fd", "lama", 2, 2), (2, "pd", "lama", 2, 2), (4, "fd", "zf", 2, 4), (4, "pd", "mrc", 2, 4)])
-def test_cluster_group_matches_single_process(tmp_path, world, arch, kind, C, bits):
+@pytest.mark.parametrize("world,arch,kind,C,bits,chunks", [
+    (2, "pd", "lmmse", 4, 4, 1), (2, "pd", "zf", 2, 4, 1), (2, "fd", "lmmse", 4, 4, 1), (2, "fd", "mrc", 2, 4, 1),
+    (2, "fd", "lama", 2, 2, 1), (2, "pd", "lama", 2, 2, 1), (4, "fd", "zf", 2, 4, 1), (4, "pd", "mrc", 2, 4, 1),
+    (2, "pd", "lmmse", 4, 4, 2), (2, "fd", "zf", 2, 4, 3)])
+def test_cluster_group_matches_single_process(tmp_path, world, arch, kind, C, bits, chunks):
+    """Every rank's finalized items (block r of every chunk) equal the
+    single-process reference path on those items."""
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, arch, kind, C, bits, str(tmp_path)), nprocs=world,
+    mp.start_processes(_worker, args=(world, port, arch, kind, C, bits, str(tmp_path), chunks), nprocs=world,
                        start_method="spawn")
     syms, _ = O.square_qam(bits)
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
-        a, b = d["items"]
+        items = d["items"]
         B = d["H"].shape[1]
         off = O.uniform_offsets(B, C)
         lp = {"t_max": 4} if kind == "lama" else None
-        ref = O.run_batch(arch, kind, d["H"], d["Y"], off, d["n0"], 1.0, syms, lp, items=range(a, b))
+        ref = O.run_batch(arch, kind, d["H"], d["Y"], off, d["n0"], 1.0, syms, lp, items=items)
         assert np.max(np.abs(d["xhat"] - ref["z"])) < 1e-10
         s2 = d["sigma2"]
         if kind == "lama":

@@ -1,8 +1,10 @@
-"""The multi-GPU code path (distributed.CudaOps: K1 stats -> NCCL
-reduce-scatter -> central solve; FD partial sums -> reduce-scatter ->
-finalize, weight all-reduce) on the one available B200 as a 1-rank NCCL group.
-Every kernel and collective call of the N-GPU path runs; the result must equal
-the fused single-GPU detector."""
+"""The multi-GPU code path (distributed.CudaOps + NcclExchange: K1 stats ->
+dbp_pd_reduce_scatter -> central solve; FD partial sums ->
+dbp_fd_reduce_scatter -> finalize, dbp_allreduce_sum of the weight sums) on
+the one available B200 as a 1-rank NCCL group.  Every kernel and collective
+call of the N-GPU path runs (also chunked, the exchange of one chunk
+overlapping the next chunk's kernels on a second stream); the result must
+equal the fused single-GPU detector."""
 
 import os
 import socket
@@ -32,10 +34,11 @@ def nccl1():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("arch,kind", [("pd", "lmmse"), ("pd", "zf"), ("pd", "lama"), ("fd", "lmmse"),
-                                       ("fd", "mrc"), ("fd", "lama")])
-def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
-    from paper_1808_04473_b200.distributed import ClusterGroup
+@pytest.mark.parametrize("arch,kind,chunks", [("pd", "lmmse", 1), ("pd", "zf", 1), ("pd", "lama", 1),
+                                              ("fd", "lmmse", 1), ("fd", "mrc", 1), ("fd", "lama", 1),
+                                              ("pd", "lmmse", 2), ("fd", "zf", 3)])
+def test_cluster_group_equals_fused(golden, nccl1, arch, kind, chunks):
+    from paper_1808_04473_b200.distributed import ClusterGroup, NcclExchange
 
     g = golden("cfg4" if kind == "lama" else "cfg2")
     const = dbp.make_constellation("qam16")
@@ -45,9 +48,11 @@ def test_cluster_group_equals_fused(golden, nccl1, arch, kind):
     n0 = torch.tensor(g["n0"], dtype=torch.float32, device="cuda")
     lp = {"t_max": 10} if kind == "lama" else None
     grp = ClusterGroup(arch, kind, [b // c] * c, u, Y.shape[1], const, lama_params=lp)
-    res = grp.run(H, Y, n0)
+    assert isinstance(grp.exchange, NcclExchange)  # the library's own NCCL entry points
+    res = grp.run(H, Y, n0, chunks=chunks)
     ref = dbp.detect(arch, kind, g["H"], g["Y"], g["n0"], [b // c] * c, const, lama_params=lp)
-    assert res.items == (0, H.shape[0])
+    assert np.array_equal(res.items, np.arange(H.shape[0]))
+    grp.close()
     # different Gram arithmetic on the two sides: the fused PD kernel uses two
     # bf16 parts per operand (~1e-5 from the float64 reference, tests/
     # test_gpu_tc2.py), the per-rank statistics three parts; the FD and LAMA
