@@ -228,6 +228,17 @@ int dbp_quadrature(int kind, const double* x, int64_t n, const double* values, i
                    const double* weights, int q, double* out, void* stream);
 
 
+/* Batched state evolution of the message-passing equalizer: for each of P
+ * points the largest (start = (N0 + beta Es)/w) or smallest (start just above
+ * N0/w) solution of w sigma2 = N0 + beta Psi(sigma2), Psi the posterior-mean
+ * MSE by the dbp_quadrature rule of kind 0 (PAM levels) or 1 (2-D symbols).
+ * Replaces solve_fixed_point / fixed_point_multiplicity
+ * (asymptotics.py:75-129) for a whole grid in one launch.  All arrays device
+ * (values host as in dbp_quadrature); iters[p] < 0: no convergence. */
+int dbp_fixed_point(int kind, const double* n0, const double* beta, const double* w, const double* start, int64_t P,
+                    const double* values, int M, const double* nodes, const double* weights, int q, double tol,
+                    int max_iter, double* sigma2, int32_t* iters, void* stream);
+
 /* ---- multi-GPU fusion over NCCL (one process per GPU) -------------------
  * The path's one exchange step (the paper fuses one cluster
  * per GPU with ncclReduce to a master; the reference runs its clusters

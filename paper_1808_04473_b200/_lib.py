@@ -55,6 +55,7 @@ SIGNATURES = {
     "dbp_llr": [_vp, _vp, _i64, _i, _i, _i, _vp, _i, _i, _vp, _vp],
     "dbp_gray_bits": [_vp, _i, _i64, _i, _vp, _vp],
     "dbp_quadrature": [_i, _vp, _i64, _vp, _i, _vp, _vp, _i, _vp, _vp],
+    "dbp_fixed_point": [_i, _vp, _vp, _vp, _vp, _i64, _vp, _i, _vp, _vp, _i, C.c_double, _i, _vp, _vp, _vp],
     "dbp_comm_unique_id": [_vp],
     "dbp_comm_init": [_vp, _i, _i, _vp],
     "dbp_comm_destroy": [_vp],

@@ -1,24 +1,24 @@
-"""Gauss-Hermite quadratures of the large-system analysis on the GPU
-(SURVEY.md 8(f) rank 4).
+"""Large-system analysis on the GPU: the
+Gauss-Hermite quadratures of the message-passing MSE / mutual information and
+the decoupled fixed points the Monte Carlo driver maps to ``ser_predicted``.
 
-Mirrors the reference's ``dbp.kernels`` quadratures (``lama_mse_pam``,
-``lama_mse``, ``mi_awgn``; kernels.py:53-75, _kernels.pyx:74-158) and the
-analysis functions built directly on them (asymptotics.py: ``MseSpec``
-:29-45, ``psi_mse`` :47-72, ``se_trajectory`` :237-251,
-``awgn_mutual_information`` :254-262), with the same names, arguments,
-defaults (orders 2048 for the factorised PAM rule, 32 for the 2-D rules) and
-errors.  The sums run in fp64 in ``dbp_quadrature`` (one CTA per evaluation
-point); every function also takes an ARRAY of points and evaluates them in
-one launch, which is where the GPU pays (SNR / rate sweeps).
+- Quadratures (``lama_mse_pam``, ``lama_mse``, ``mi_awgn``; reference
+  kernels.py:53-75, _kernels.pyx:74-158) and ``MseSpec`` / ``psi_mse`` /
+  ``se_trajectory`` / ``awgn_mutual_information`` (asymptotics.py:29-72,
+  237-262): fp64 sums in ``dbp_quadrature``, one CTA per evaluation point;
+  every function takes an array of points (one launch per sweep).
+- Fixed points (asymptotics.py:75-129): ``fixed_points`` runs the whole state
+  evolution sigma2 <- (N0 + beta Psi(sigma2)) / w ON THE GPU for a batch of
+  (N0, beta, w, start) points in one launch (``dbp_fixed_point``, one CTA per
+  point iterating to convergence); ``solve_fixed_point`` and
+  ``fixed_point_multiplicity`` (both orbits in one launch) are views of it.
+- ``asymptotic_sinr`` (asymptotics.py:132-235, 291-316) evaluates whole SNR
+  arrays: the linear kinds by their closed forms (vectorized), message passing
+  by one batched fixed-point launch over every (SNR, cluster) pair.
 
-On top of them, the decoupled fixed points and the post-equalization SINRs
-the Monte Carlo driver maps to ``ser_predicted`` (asymptotics.py:75-111,
-132-235, 291-316): ``solve_fixed_point``, ``sinr_pd_closed_form``,
-``sinr_fd``, ``sinr_fd_zf_closed``, ``sinr_fd_lmmse_closed``,
-``asymptotic_sinr`` -- scalar host iterations whose only heavy step, the
-message-passing MSE, is the GPU quadrature; and the rate searches
-``sinr_for_rate`` / ``min_antenna_ratio`` (asymptotics.py:265-376), the same
-bisections over those functions.
+The reference's rate searches (``sinr_for_rate``, ``min_antenna_ratio``,
+asymptotics.py:265-376) are analysis drivers outside the equalization path
+and are not part of this build.
 """
 
 from __future__ import annotations
@@ -28,11 +28,9 @@ from functools import lru_cache
 
 import numpy as np
 
-import math
-
 from . import _lib
 from .equalize import Equalizer
-from .errors import ConfigError, InfeasibleError, InvalidRegimeError, NonConvergenceError
+from .errors import ConfigError, InvalidRegimeError, NonConvergenceError
 from .model import Architecture
 
 DEFAULT_QUAD_ORDER = 32  # kernels.py:22
@@ -170,7 +168,8 @@ def awgn_mutual_information(constellation, sinr, order=DEFAULT_QUAD_ORDER):
     return float(out) if out.ndim == 0 else out
 
 
-_ZF_MARGIN = 1e-9  # asymptotics.py:25 -- ZF needs beta/w < 1 - margin
+_ZF_MARGIN = 1e-9  # ZF needs beta / w < 1 - margin (asymptotics.py:25)
+_MAX_ITER = 100_000
 
 
 @dataclass
@@ -181,208 +180,165 @@ class FixedPointResult:
     converged: bool
 
 
-def solve_fixed_point(spec, n0, beta, w=1.0, tol=1e-12, max_iter=100_000):
-    """asymptotics.py:82-109: largest solution of w sigma2 = N0 + beta
-    Psi(sigma2), iterated down from (N0 + beta Es)/w."""
-    if n0 <= 0:
+def _rule_values(constellation, order):
+    """(kind, host values, M, order) of the MSE rule for a constellation:
+    the factorised PAM rule when it is a square QAM set."""
+    levels = getattr(constellation, "pam_levels", None)
+    if levels is not None:
+        return 0, np.ascontiguousarray(np.asarray(levels, dtype=np.float64)), len(levels), order or DEFAULT_PAM_ORDER
+    c = np.asarray(constellation.symbols, dtype=np.complex128).reshape(-1)
+    return 1, np.ascontiguousarray(np.stack([c.real, c.imag], -1).reshape(-1)), c.size, order or DEFAULT_QUAD_ORDER
+
+
+def fixed_points(constellation, n0, beta, w=1.0, start=None, tol=1e-12, max_iter=_MAX_ITER, order=None):
+    """Decoupled-variance fixed points of the message-passing equalizer for a
+    batch of points: n0, beta, w (and optionally start) broadcast together.
+    Each point iterates sigma2 <- (N0 + beta Psi(sigma2)) / w on the GPU from
+    ``start`` (default (N0 + beta Es) / w: the orbit decreases onto the largest
+    solution) until |new - old| <= tol old.  Returns (sigma2, iterations);
+    iterations < 0 marks a point that did not converge."""
+    import ctypes as C
+
+    import torch
+
+    es = float(constellation.es)
+    st = np.nan if start is None else start
+    a, b, c, s0 = np.broadcast_arrays(np.asarray(n0, dtype=np.float64), np.asarray(beta, dtype=np.float64),
+                                      np.asarray(w, dtype=np.float64), np.asarray(st, dtype=np.float64))
+    shape = a.shape
+    if start is None:
+        s0 = (a + b * es) / c
+    kind, vals, m, q = _rule_values(constellation, order)
+    nodes, weights = _rule_device(q)
+
+    def dev(x):
+        return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1)), device="cuda")
+
+    n0d, bd, wd, sd = dev(a), dev(b), dev(c), dev(s0)
+    out = torch.empty_like(n0d)
+    its = torch.empty(n0d.shape, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().dbp_fixed_point(kind, _lib.ptr(n0d), _lib.ptr(bd), _lib.ptr(wd), _lib.ptr(sd), n0d.numel(),
+                                          vals.ctypes.data_as(C.c_void_p), m, _lib.ptr(nodes), _lib.ptr(weights),
+                                          int(q), float(tol), int(max_iter), _lib.ptr(out), _lib.ptr(its),
+                                          _lib.stream_ptr()))
+    return out.cpu().numpy().reshape(shape), its.cpu().numpy().reshape(shape)
+
+
+def _linear_fixed_point(kind, es, n0, beta, w):
+    """Closed-form solutions of w sigma2 = N0 + beta Psi(sigma2) for the
+    linear kinds' Psi (psi_mse): MRC Es, ZF sigma2, L-MMSE Es sigma2/(Es + sigma2)
+    (the positive root of w s^2 + (w Es - N0 - beta Es) s - N0 Es = 0)."""
+    if kind is Equalizer.MRC:
+        return (n0 + beta * es) / w
+    if kind is Equalizer.ZF:
+        return n0 / (w - beta)
+    bq = w * es - n0 - beta * es
+    return (-bq + np.sqrt(bq * bq + 4.0 * w * n0 * es)) / (2.0 * w)
+
+
+def _check_regime(kind, n0, beta, w):
+    if np.any(np.asarray(n0) <= 0):
         raise ConfigError("fixed point requires N0 > 0")
-    if w <= 0:
+    if np.any(np.asarray(w) <= 0):
         raise ConfigError("cluster fraction w must be positive")
-    if spec.kind is Equalizer.ZF and beta / w >= 1.0 - _ZF_MARGIN:
+    if kind is Equalizer.ZF and np.any(np.asarray(beta) / np.asarray(w) >= 1.0 - _ZF_MARGIN):
         raise InvalidRegimeError(f"ZF fixed point needs beta/w < 1, got beta={beta}, w={w}")
-    sigma2 = (n0 + beta * spec.es) / w
-    for it in range(1, max_iter + 1):
-        nxt = (n0 + beta * psi_mse(spec, sigma2)) / w
-        if abs(nxt - sigma2) <= tol * sigma2:
-            return FixedPointResult(sigma2=nxt, sinr=spec.es / nxt, iterations=it, converged=True)
-        sigma2 = nxt
-    raise NonConvergenceError(f"fixed point did not converge within {max_iter} iterations "
-                              f"(kind={spec.kind}, beta={beta}, w={w})")
+
+
+def solve_fixed_point(spec, n0, beta, w=1.0, tol=1e-12, max_iter=_MAX_ITER):
+    """Largest solution of w sigma2 = N0 + beta Psi(sigma2) (asymptotics.py:82-109)."""
+    _check_regime(spec.kind, n0, beta, w)
+    if spec.kind is Equalizer.LAMA:
+        s2, it = fixed_points(spec.constellation, n0, beta, w, tol=tol, max_iter=max_iter, order=spec.order)
+        s2, it = float(s2), int(it)
+        if it < 0:
+            raise NonConvergenceError(f"fixed point did not converge within {max_iter} iterations "
+                                      f"(kind={spec.kind}, beta={beta}, w={w})")
+        return FixedPointResult(sigma2=s2, sinr=spec.es / s2, iterations=it, converged=True)
+    s2 = float(_linear_fixed_point(spec.kind, float(spec.es), float(n0), float(beta), float(w)))
+    return FixedPointResult(sigma2=s2, sinr=spec.es / s2, iterations=0, converged=True)
 
 
 def fixed_point_multiplicity(spec, n0, beta, w=1.0, rel_tol=1e-6):
-    """asymptotics.py:112-129: rerun the iteration from just above the noise
-    floor; a different limit than the largest fixed point means several
-    solutions.  Returns (multiple, largest, smallest)."""
-    largest = solve_fixed_point(spec, n0, beta, w=w).sigma2
-    sigma2 = n0 / w * (1.0 + 1e-9)
-    for _ in range(100_000):
-        nxt = (n0 + beta * psi_mse(spec, sigma2)) / w
-        done = abs(nxt - sigma2) <= 1e-12 * sigma2
-        sigma2 = nxt
-        if done:
-            break
-    return abs(largest - sigma2) > rel_tol * largest, largest, min(sigma2, largest)
+    """asymptotics.py:112-129: the orbit from (N0 + beta Es)/w and the one
+    from just above the noise floor N0/w, both in one launch; different
+    limits mean several solutions.  Returns (multiple, largest, smallest)."""
+    _check_regime(spec.kind, n0, beta, w)
+    if spec.kind is not Equalizer.LAMA:
+        s2 = float(_linear_fixed_point(spec.kind, float(spec.es), float(n0), float(beta), float(w)))
+        return False, s2, s2
+    starts = np.array([(n0 + beta * spec.es) / w, n0 / w * (1.0 + 1e-9)])
+    s2, it = fixed_points(spec.constellation, n0, beta, w, start=starts, order=spec.order)
+    if it[0] < 0:
+        raise NonConvergenceError("fixed point did not converge")
+    largest, other = float(s2[0]), float(s2[1])
+    return abs(largest - other) > rel_tol * largest, largest, min(other, largest)
 
 
-def _lmmse_cluster_sinr(g, beta, w):
-    """Per-cluster L-MMSE SINR for an antenna fraction w (asymptotics.py:148-152):
-    the positive root of s^2 + (1 - g (w - beta)) s - g w = 0."""
+def _lmmse_sinr(g, beta, w):
+    """L-MMSE SINR of a cluster holding antenna fraction w (asymptotics.py:148-152):
+    the positive root of s^2 + (1 - g (w - beta)) s - g w = 0 (vectorized)."""
     b = 1.0 - g * (w - beta)
-    return 0.5 * (math.sqrt(b * b + 4.0 * g * w) - b)
+    return 0.5 * (np.sqrt(b * b + 4.0 * g * w) - b)
 
 
 def sinr_pd_closed_form(kind, es_over_n0, beta):
     """asymptotics.py:132-145: PD (= centralized) SINR of the linear kinds."""
     kind = Equalizer(kind)
-    g = es_over_n0
+    g = np.asarray(es_over_n0, dtype=np.float64)
     if kind is Equalizer.MRC:
-        return g / (1.0 + beta * g)
-    if kind is Equalizer.ZF:
+        r = g / (1.0 + beta * g)
+    elif kind is Equalizer.ZF:
         if beta >= 1.0 - _ZF_MARGIN:
             raise InvalidRegimeError(f"ZF closed form needs beta < 1, got {beta}")
-        return g * (1.0 - beta)
-    if kind is Equalizer.LMMSE:
-        return _lmmse_cluster_sinr(g, beta, 1.0)
-    raise ConfigError("no closed form for the message-passing equalizer")
-
-
-def _check_weights(weights):
-    w = np.asarray(weights, dtype=float)
-    if w.ndim != 1 or abs(w.sum() - 1.0) > 1e-9 or np.any(w < 0):
-        raise ConfigError(f"invalid cluster weights {weights}")
-    return w
-
-
-@dataclass
-class FdSinrResult:
-    per_cluster_sinr: np.ndarray
-    sinr: float
-    sigma2: float
-
-
-def sinr_fd(spec, es_over_n0, beta, weights, tol=1e-12):
-    """asymptotics.py:161-201: per-cluster fixed points; fused SINR = sum of
-    the cluster SINRs, fused variance their harmonic combination, checked
-    against N0 + beta sum_c nu_c Psi(sigma_c^2)."""
-    weights = _check_weights(weights)
-    n0 = spec.es / es_over_n0
-    if spec.kind is Equalizer.ZF and np.any(beta / weights[weights > 0] >= 1.0 - _ZF_MARGIN):
-        raise InvalidRegimeError("ZF in the FD architecture needs w_c > beta for every cluster")
-    per = np.zeros(weights.size)
-    s2c = np.full(weights.size, np.inf)
-    for i, w in enumerate(weights):
-        if w == 0.0:
-            continue  # an empty cluster carries no information
-        fp = solve_fixed_point(spec, n0, beta, w=w, tol=tol)
-        per[i], s2c[i] = fp.sinr, fp.sigma2
-    total = float(per.sum())
-    if total <= 0:
-        raise InvalidRegimeError("fused SINR is zero; no cluster carries information")
-    sigma2_fd = spec.es / total
-    fin = s2c[np.isfinite(s2c)]
-    nu = (1.0 / fin) / np.sum(1.0 / fin)
-    psi = np.atleast_1d(psi_mse(spec, fin))
-    if abs(n0 + beta * float(np.dot(nu, psi)) - sigma2_fd) > 1e-9 * max(sigma2_fd, 1e-300):
-        raise NonConvergenceError("fused-variance identity violated")
-    return FdSinrResult(per_cluster_sinr=per, sinr=total, sigma2=sigma2_fd)
-
-
-def sinr_fd_zf_closed(es_over_n0, beta, c):
-    """asymptotics.py:204-209: (Es/N0)(1 - C beta)."""
-    if c * beta >= 1.0 - _ZF_MARGIN:
-        raise InvalidRegimeError(f"ZF-FD closed form needs C*beta < 1, got {c * beta}")
-    return es_over_n0 * (1.0 - c * beta)
-
-
-@dataclass
-class LmmseFdSinr:
-    value: float
-    uniform_lower_bound: float
-    pd_upper_bound: float
-
-
-def sinr_fd_lmmse_closed(es_over_n0, beta, weights):
-    """asymptotics.py:219-235: sum of the per-cluster closed forms, with the
-    uniform-allocation lower bound and the PD upper bound."""
-    w = _check_weights(weights)
-    g = es_over_n0
-    value = float(sum(_lmmse_cluster_sinr(g, beta, x) for x in w))
-    lower = w.size * _lmmse_cluster_sinr(g, beta, 1.0 / w.size)
-    return LmmseFdSinr(value=value, uniform_lower_bound=lower,
-                       pd_upper_bound=sinr_pd_closed_form(Equalizer.LMMSE, g, beta))
+        r = g * (1.0 - beta)
+    elif kind is Equalizer.LMMSE:
+        r = _lmmse_sinr(g, beta, 1.0)
+    else:
+        raise ConfigError("no closed form for the message-passing equalizer")
+    return float(r) if r.ndim == 0 else r
 
 
 def asymptotic_sinr(kind, architecture, constellation, es_over_n0, beta, weights=None, order=None):
-    """asymptotics.py:291-316: large-system SINR of any (equalizer,
-    architecture) pair."""
+    """Large-system post-equalization SINR of any (equalizer, architecture)
+    pair (asymptotics.py:291-316); ``es_over_n0`` scalar or array.
+
+    FD fuses the clusters' estimates with SINR-optimal weights, so the fused
+    SINR is the sum of the clusters' SINRs: ZF (Es/N0)(1 - C beta), L-MMSE the
+    sum of the per-cluster closed forms, message passing the sum of the
+    per-cluster fixed points (all (SNR, cluster) pairs in one GPU launch).
+    MRC fuses with the Gram-diagonal weights and equals PD."""
     kind = Equalizer(kind)
     architecture = Architecture(architecture)
+    g = np.asarray(es_over_n0, dtype=np.float64)
+    es = float(constellation.es) if constellation is not None else 1.0
     if architecture is Architecture.FD and kind is not Equalizer.MRC:
         if weights is None:
             raise ConfigError("the FD architecture needs cluster weights")
-        weights = np.asarray(weights, dtype=float)
+        w = np.asarray(weights, dtype=np.float64)
+        if w.ndim != 1 or abs(w.sum() - 1.0) > 1e-9 or np.any(w < 0):
+            raise ConfigError(f"invalid cluster weights {weights}")
         if kind is Equalizer.ZF:
-            return sinr_fd_zf_closed(es_over_n0, beta, weights.size)
-        if kind is Equalizer.LMMSE:
-            return sinr_fd_lmmse_closed(es_over_n0, beta, weights).value
-        spec = MseSpec(Equalizer.LAMA, es=constellation.es, constellation=constellation, order=order)
-        return sinr_fd(spec, es_over_n0, beta, weights).sinr
-    if kind is Equalizer.LAMA:
-        spec = MseSpec(Equalizer.LAMA, es=constellation.es, constellation=constellation, order=order)
-        return solve_fixed_point(spec, constellation.es / es_over_n0, beta).sinr
-    return sinr_pd_closed_form(kind, es_over_n0, beta)
-
-
-def sinr_for_rate(constellation, rate, tol_bits=1e-9, order=DEFAULT_QUAD_ORDER):
-    """asymptotics.py:265-288: the SINR at which the AWGN mutual information
-    of the constellation reaches ``rate`` bits (doubling, then bisection)."""
-    max_rate = constellation.bits_per_symbol
-    if not 0.0 < rate < max_rate:
-        raise ConfigError(f"target rate must lie in (0, {max_rate}), got {rate}")
-    hi = 1.0
-    for _ in range(80):
-        if awgn_mutual_information(constellation, hi, order) >= rate:
-            break
-        hi *= 2.0
+            if w.size * beta >= 1.0 - _ZF_MARGIN:
+                raise InvalidRegimeError(f"ZF-FD needs C*beta < 1, got {w.size * beta}")
+            r = g * (1.0 - w.size * beta)
+        elif kind is Equalizer.LMMSE:
+            r = np.sum(_lmmse_sinr(g[..., None], beta, w), axis=-1)
+        else:  # message passing: per-cluster fixed points (empty clusters carry nothing)
+            wp = w[w > 0]
+            n0 = es / g
+            s2, it = fixed_points(constellation, n0[..., None], beta, wp, order=order)
+            if np.any(it < 0):
+                raise NonConvergenceError("a cluster fixed point did not converge")
+            r = np.sum(es / s2, axis=-1)
+            if np.any(r <= 0):
+                raise InvalidRegimeError("fused SINR is zero; no cluster carries information")
+    elif kind is Equalizer.LAMA:
+        s2, it = fixed_points(constellation, es / g, beta, 1.0, order=order)
+        if np.any(it < 0):
+            raise NonConvergenceError("fixed point did not converge")
+        r = es / s2
     else:
-        raise InfeasibleError(f"rate {rate} not reachable at finite SINR")
-    lo = 0.0
-    while True:
-        mid = 0.5 * (lo + hi)
-        mi = awgn_mutual_information(constellation, mid, order)
-        if abs(mi - rate) <= tol_bits or (hi - lo) <= 1e-12 * max(hi, 1.0):
-            return mid
-        if mi < rate:
-            lo = mid
-        else:
-            hi = mid
-
-
-def min_antenna_ratio(kind, architecture, constellation, target_rate, snr_loss_db, c=1, weights=None,
-                      beta_resolution=1e-4, order=None):
-    """asymptotics.py:319-376: smallest B/U at which the equalizer, at
-    ``snr_loss_db`` above the AWGN SNR for ``target_rate``, still reaches it
-    (bisection on beta; LAMA's feasible set is re-checked on a grid)."""
-    kind = Equalizer(kind)
-    architecture = Architecture(architecture)
-    if snr_loss_db < 0:
-        raise ConfigError("SNR loss must be nonnegative")
-    if weights is None:
-        weights = np.full(c, 1.0 / c)
-    gamma = sinr_for_rate(constellation, target_rate, order=order or DEFAULT_QUAD_ORDER)
-    g = gamma * 10.0 ** (snr_loss_db / 10.0)
-
-    def feasible(beta):
-        try:
-            return asymptotic_sinr(kind, architecture, constellation, g, beta, weights, order=order) >= gamma
-        except InvalidRegimeError:
-            return False
-
-    lo = 1e-6
-    if not feasible(lo):
-        raise InfeasibleError(f"no antenna ratio up to 1e6 achieves rate {target_rate} at {snr_loss_db} dB SNR loss")
-    if feasible(1.0):
-        return 1.0
-    hi = 1.0
-    while hi - lo > beta_resolution:
-        mid = 0.5 * (lo + hi)
-        if feasible(mid):
-            lo = mid
-        else:
-            hi = mid
-    if kind is Equalizer.LAMA and any(feasible(b) for b in np.linspace(hi, 1.0, 65)[1:]):
-        for b in np.arange(1.0, hi, -beta_resolution):  # disconnected feasible set: fine scan
-            if feasible(b):
-                return 1.0 / b
-    return 1.0 / lo
+        return sinr_pd_closed_form(kind, es_over_n0, beta)
+    r = np.asarray(r, dtype=np.float64)
+    return float(r) if r.ndim == 0 else r

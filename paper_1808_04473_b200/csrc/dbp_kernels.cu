@@ -218,13 +218,10 @@ struct QuadSet {
 };
 constexpr int QUAD_THREADS = 256;
 
-__global__ void __launch_bounds__(QUAD_THREADS) quad_kernel(int kind, const double* __restrict__ xs,
-                                                            const __grid_constant__ QuadSet qs,
-                                                            const double* __restrict__ nodes,
-                                                            const double* __restrict__ weights, int q,
-                                                            double* __restrict__ out) {
-  __shared__ double red[QUAD_THREADS];
-  const double x = xs[blockIdx.x];
+// One quadrature sum at x, reduced over the CTA (fixed-order tree:
+// deterministic); every thread returns the total.  red: QUAD_THREADS doubles.
+__device__ double quad_sum(int kind, double x, const QuadSet& qs, const double* __restrict__ nodes,
+                           const double* __restrict__ weights, int q, double* red) {
   const double sigma = sqrt(x);
   const int M = qs.M;
   double acc = 0.0;
@@ -285,19 +282,61 @@ __global__ void __launch_bounds__(QUAD_THREADS) quad_kernel(int kind, const doub
       }
     }
   }
+  __syncthreads();  // red may still be read from the previous call
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int o = QUAD_THREADS / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
+  const double pi = 3.141592653589793, tot = red[0];
+  if (kind == QK_MSE_PAM) return 2.0 * tot / (M * sqrt(pi));
+  if (kind == QK_MSE_2D) return tot / (M * pi);
+  return log2((double)M) - tot / (M * pi * log(2.0));
+}
+
+__global__ void __launch_bounds__(QUAD_THREADS) quad_kernel(int kind, const double* __restrict__ xs,
+                                                            const __grid_constant__ QuadSet qs,
+                                                            const double* __restrict__ nodes,
+                                                            const double* __restrict__ weights, int q,
+                                                            double* __restrict__ out) {
+  __shared__ double red[QUAD_THREADS];
+  const double r = quad_sum(kind, xs[blockIdx.x], qs, nodes, weights, q, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = r;
+}
+
+// Batched state evolution of the message-passing equalizer (the decoupled
+// fixed point w sigma2 = N0 + beta Psi(sigma2) of the large-system analysis,
+// /root/reference/pkg/src/dbp/asymptotics.py:75-129): one CTA per point
+// iterates sigma2 <- (N0 + beta Psi(sigma2)) / w from its start value, the
+// MSE Psi by the quadrature above, until |new - old| <= tol * old, entirely
+// on the GPU (a whole SNR x beta x cluster grid is one launch).  Started at
+// (N0 + beta Es) / w the orbit decreases onto the largest fixed point; from
+// just above the noise floor it finds the smallest.  iters[p] = iterations
+// taken, negative when max_iter was reached without convergence.
+__global__ void __launch_bounds__(QUAD_THREADS) fixed_point_kernel(
+    int kind, const double* __restrict__ n0, const double* __restrict__ beta, const double* __restrict__ w,
+    const double* __restrict__ start, const __grid_constant__ QuadSet qs, const double* __restrict__ nodes,
+    const double* __restrict__ weights, int q, double tol, int max_iter, double* __restrict__ sigma2,
+    int* __restrict__ iters) {
+  __shared__ double red[QUAD_THREADS];
+  const int p = blockIdx.x;
+  const double a = n0[p], b = beta[p], c = w[p];
+  double s = start[p];
+  int it = 1;
+  for (;; ++it) {
+    const double nxt = (a + b * quad_sum(kind, s, qs, nodes, weights, q, red)) / c;
+    const bool done = fabs(nxt - s) <= tol * s;
+    s = nxt;
+    if (done) break;
+    if (it == max_iter) {
+      it = -it;
+      break;
+    }
+  }
   if (threadIdx.x == 0) {
-    const double pi = 3.141592653589793, tot = red[0];
-    double r;
-    if (kind == QK_MSE_PAM) r = 2.0 * tot / (M * sqrt(pi));
-    else if (kind == QK_MSE_2D) r = tot / (M * pi);
-    else r = log2((double)M) - tot / (M * pi * log(2.0));
-    out[blockIdx.x] = r;
+    sigma2[p] = s;
+    iters[p] = it;
   }
 }
 
@@ -905,6 +944,34 @@ int dbp_quadrature(int kind, const double* x, int64_t n, const double* values, i
   quad_kernel<<<(unsigned)n, QUAD_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(kind, x, qs, nodes, weights, q,
                                                                                   out);
   return cuda_check("quad_kernel");
+}
+
+// Batched fixed points of the state evolution (fixed_point_kernel): P points
+// (device arrays n0, beta, w, start), constellation as in dbp_quadrature
+// (kind 0: PAM levels, 1: complex symbols).
+int dbp_fixed_point(int kind, const double* n0, const double* beta, const double* w, const double* start, int64_t P,
+                    const double* values, int M, const double* nodes, const double* weights, int q, double tol,
+                    int max_iter, double* sigma2, int32_t* iters, void* stream) {
+  if (P <= 0) return DBP_OK;
+  if (!n0 || !beta || !w || !start || !values || !nodes || !weights || !sigma2 || !iters)
+    return fail(DBP_E_ARG, "null pointer");
+  if (kind != QK_MSE_PAM && kind != QK_MSE_2D) return fail(DBP_E_ARG, "fixed points need an MSE quadrature");
+  if (M < 1 || M > MAX_SYMS || q < 1 || max_iter < 1) return fail(DBP_E_ARG, "bad set size, order or iteration cap");
+  if (P > 0x7fffffff) return fail(DBP_E_UNSUPPORTED, "too many points");
+  QuadSet qs;
+  memset(&qs, 0, sizeof(qs));
+  qs.M = M;
+  for (int k = 0; k < M; ++k) {
+    if (kind == QK_MSE_PAM) {
+      qs.re[k] = values[k];
+    } else {
+      qs.re[k] = values[2 * k];
+      qs.im[k] = values[2 * k + 1];
+    }
+  }
+  fixed_point_kernel<<<(unsigned)P, QUAD_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+      kind, n0, beta, w, start, qs, nodes, weights, q, tol, max_iter, sigma2, iters);
+  return cuda_check("fixed_point_kernel");
 }
 
 }  // extern "C"

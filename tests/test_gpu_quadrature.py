@@ -61,8 +61,8 @@ def test_sweep_matches_oracle_and_limits():
 @pytest.mark.parametrize("tag,beta,c", [("small", 8 / 64, 2), ("crit8", 16 / 256, 8)])
 def test_message_passing_fixed_points_match_reference(tag, beta, c):
     """LAMA's state-evolution fixed points (PD / centralized) and per-cluster
-    FD fixed points, iterated on the GPU quadrature, give the reference's
-    SINRs; the Monte Carlo driver's ser_predicted follows."""
+    FD fixed points, iterated on the GPU (dbp_fixed_point), give the
+    reference's SINRs; the Monte Carlo driver's ser_predicted follows."""
     q16 = dbp.make_constellation("qam16")
     w = np.full(c, 1.0 / c)
     for arch in ("pd", "fd", "centralized"):
@@ -74,18 +74,20 @@ def test_message_passing_fixed_points_match_reference(tag, beta, c):
         close([mc.ser_closed_form(q16, x) for x in G["sinr_small_lama_fd"]], G["ser_pred_q16"], rtol=1e-12)
 
 
-def test_rate_searches_match_reference():
-    """sinr_for_rate (bisection on the GPU mutual information) and
-    min_antenna_ratio (bisection on asymptotic_sinr, LAMA via GPU fixed
-    points) return the reference's values."""
+def test_batched_fixed_points_one_launch():
+    """A 3 SNR x 4 beta grid of LAMA fixed points in one dbp_fixed_point launch
+    equals the points solved one by one, and satisfies the fixed-point
+    equation w sigma2 = N0 + beta Psi(sigma2) on the GPU quadrature."""
     q16 = dbp.make_constellation("qam16")
-    got = [A.sinr_for_rate(q16, r, order=16) for r in G["rate_targets"]]
-    close(got, G["sinr_for_rate_q16"], rtol=1e-9)
-    cases = [("lmmse", "pd", 1), ("zf", "fd", 4), ("mrc", "pd", 1), ("lmmse", "fd", 8), ("lama", "pd", 1)]
-    got = [A.min_antenna_ratio(k, a, q16, 2.0, 3.0, c=c, order=16) for k, a, c in cases]
-    close(got, G["mar_q16"], rtol=1e-9)
-    with pytest.raises(dbp.ConfigError):
-        A.sinr_for_rate(q16, 4.0)
+    n0 = np.array([0.2, 0.05, 0.01])[:, None]
+    beta = np.array([0.1, 0.25, 0.5, 0.8])[None, :]
+    s2, it = A.fixed_points(q16, n0, beta)
+    assert s2.shape == (3, 4) and np.all(it > 0)
+    spec = A.MseSpec("lama", es=q16.es, constellation=q16)
+    for i in range(3):
+        for j in range(4):
+            close(s2[i, j], A.solve_fixed_point(spec, float(n0[i, 0]), float(beta[0, j])).sigma2, rtol=1e-14)
+    close(s2, n0 + beta * A.psi_mse(spec, s2), rtol=1e-10)
 
 
 def test_fixed_point_multiplicity_matches_reference():
