@@ -35,7 +35,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <int MODE, int NSPLIT>
 static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm, const CUtensorMap& ym,
                            cudaStream_t st) {
-  const bool fd = MODE == T2_FD || MODE == T2_FD_MRC;
+  const bool fd = MODE == T2_FD;
   const Tc2Layout L = make_tc2_layout(g, p.TP, p.C, fd);
   int dev = 0, smem_max = 0;
   cudaGetDevice(&dev);
@@ -44,8 +44,7 @@ static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm,
   auto kern = tc2_kernel<MODE, NSPLIT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
-  const int gpi = g.upi > 4 ? g.upi / 4 : 1;  // groups per item (CTAs own whole items)
-  const int64_t grid = std::min<int64_t>(g.G_tot / gpi, (int64_t)sm_count());
+  const int64_t grid = std::min<int64_t>(g.G_tot / g.upi, (int64_t)sm_count());  // CTAs own whole item blocks
 #ifdef DBP_STUDY
   static long long* dbg = nullptr;
   const bool debug = getenv("DBP_TC_DEBUG") != nullptr;
@@ -76,7 +75,6 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   const bool per_cluster = fdm || (p.arch == ARCH_STATS && !p.sum_clusters);
   if (p.kind == EQ_LAMA || p.u > 16 || p.us > 16 || p.T > 16) return 1;
   const int upi = per_cluster ? p.C : 1;
-  if (!(upi == 1 || upi == 2 || upi % 4 == 0)) return 1;
   if (p.B % upi) return 1;
   const int K = p.B / upi;
   for (int c = 0; c < upi && per_cluster; ++c) {  // uniform contiguous clusters only
@@ -89,6 +87,7 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
     if (rows != K) return 1;
   }
   if ((reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y)) & 15) return 1;
+  if (p.n_items > 0x7ffffff0) return 1;  // TMA coordinates are int32
   auto enc = tensor_map_encoder();
   if (!enc) return 1;
   Tc2Geom g;
@@ -96,34 +95,34 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   g.K = K;
   g.nchunk = (K + 31) / 32;
   g.upi = upi;
-  g.gc = upi >= 4 ? 4 : upi;
-  g.gn = 4 / g.gc;
   g.us = p.us;
   g.T = p.T;
-  g.U_tot = p.n_items * upi;
-  g.G_tot = (g.U_tot + 3) / 4;
+  g.n_items = p.n_items;
+  g.G_tot = (p.n_items + 3) / 4 * upi;
   g.hbytes = 4 * 32 * 2 * p.us * 4;
-  g.lean = (p.kind == EQ_MRC && p.arch != ARCH_STATS) ? 2 : 1;
-  g.ybox = g.gn * p.T * T2_YROW * 4;
-  g.ystride = align_up(g.ybox, 128);
+  g.ybox = 4 * p.T * T2_YROW * 4;
+  g.lean = 1;
   const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : (p.arch == ARCH_PD) ? 2 : 3;
   if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
-  const int raw = g.hbytes + g.gc * g.ystride;
+  const int raw = g.hbytes + g.ybox;
   g.stage_bytes = align_up(std::max(raw, nsplit * T2_SPLIT_BYTES), 1024);
   CUtensorMap hm, ym;
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)2 * p.us, (cuuint64_t)K, (cuuint64_t)g.U_tot};
-    const cuuint64_t strides[2] = {(cuuint64_t)2 * p.us * 4, (cuuint64_t)K * 2 * p.us * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)2 * p.us, 32, 4}, es[3] = {1, 1, 1};
-    if (enc(&hm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(p.H), dims, strides, box, es,
+    // H as [item][cluster][antenna][2 us floats]; box = 4 items x 1 cluster x 32 antennas
+    const cuuint64_t dims[4] = {(cuuint64_t)2 * p.us, (cuuint64_t)K, (cuuint64_t)upi, (cuuint64_t)p.n_items};
+    const cuuint64_t strides[3] = {(cuuint64_t)2 * p.us * 4, (cuuint64_t)K * 2 * p.us * 4,
+                                   (cuuint64_t)p.B * 2 * p.us * 4};
+    const cuuint32_t box[4] = {(cuuint32_t)2 * p.us, 32, 1, 4}, es[4] = {1, 1, 1, 1};
+    if (enc(&hm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float2*>(p.H), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return 1;
   }
   {
+    // Y as [item][T][cluster][2K floats]; box = 4 items x T x 1 cluster x (32 antennas + 2 of padding)
     const cuuint64_t dims[4] = {(cuuint64_t)2 * K, (cuuint64_t)upi, (cuuint64_t)p.T, (cuuint64_t)p.n_items};
     const cuuint64_t strides[3] = {(cuuint64_t)2 * K * 4, (cuuint64_t)2 * p.B * 4, (cuuint64_t)2 * p.T * p.B * 4};
-    const cuuint32_t box[4] = {T2_YROW, 1, (cuuint32_t)p.T, (cuuint32_t)g.gn}, es[4] = {1, 1, 1, 1};
+    const cuuint32_t box[4] = {T2_YROW, 1, (cuuint32_t)p.T, 4}, es[4] = {1, 1, 1, 1};
     if (enc(&ym, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float2*>(p.Y), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -142,21 +141,9 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
       break;
     }
   }
-  if (fdm) {  // per-(item, cluster) fold records: L2-resident scratch
-    const size_t need = (size_t)p.n_items * p.C * fd_record_floats(p.u, p.T, p.u) * sizeof(float);
-    p.fd_scratch = static_cast<float*>(stream_scratch(st, need));
-    if (!p.fd_scratch) return fail(DBP_E_CUDA, "FD scratch allocation failed");
-  }
   if (p.arch == ARCH_STATS) return nsplit == 2 ? launch_tc2_mode<T2_STATS, 2>(p, g, hm, ym, st)
                                                : launch_tc2_mode<T2_STATS, 3>(p, g, hm, ym, st);
-  const bool mrc = p.kind == EQ_MRC;
-  if (fdm) {
-    if (mrc) return nsplit == 2 ? launch_tc2_mode<T2_FD_MRC, 2>(p, g, hm, ym, st)
-                                : launch_tc2_mode<T2_FD_MRC, 3>(p, g, hm, ym, st);
-    return nsplit == 2 ? launch_tc2_mode<T2_FD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3>(p, g, hm, ym, st);
-  }
-  if (mrc) return nsplit == 2 ? launch_tc2_mode<T2_PD_MRC, 2>(p, g, hm, ym, st)
-                              : launch_tc2_mode<T2_PD_MRC, 3>(p, g, hm, ym, st);
+  if (fdm) return nsplit == 2 ? launch_tc2_mode<T2_FD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3>(p, g, hm, ym, st);
   return nsplit == 2 ? launch_tc2_mode<T2_PD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_PD, 3>(p, g, hm, ym, st);
 }
 

@@ -19,10 +19,10 @@
 // m.m + h.l + l.h (NSPLIT = 3: ~3xTF32 accuracy, for ill-conditioned FD-ZF).
 // Plain TF32 would miss the 1e-4 tolerance.
 //
-// Stage = 4 units x 32 antennas: the TMA (tensor maps, zero fill past the
-// unit's antennas / the last unit) lands H as [unit][32 antennas][2U floats]
-// and Y as [cluster][item][T][68 floats] (4 floats of row padding so the
-// converter's column reads spread over all banks).  The converter warps load
+// Stage = 4 units (cluster c of 4 consecutive items) x 32 antennas: the TMA
+// (tensor maps, zero fill past the unit's antennas / the last item) lands H
+// as [item][32 antennas][2U floats] and Y as [item][T][68 floats] (4 floats
+// of row padding so the converter's column reads spread over all banks).  The converter warps load
 // the whole stage into registers, meet at a named barrier, and write the bf16
 // splits IN PLACE as MN-major, 128-byte-swizzled operand tiles
 // ([split][4 MN blocks of 64 features][32 K rows of 128 B], 16-byte chunk j of
@@ -85,30 +85,34 @@ constexpr int T2_FD_CNT = 64;
 
 // one kernel per epilogue class, so each binary carries only its own solver
 // code (instruction-cache footprint)
-enum { T2_STATS = 0, T2_PD = 1, T2_FD = 2, T2_PD_MRC = 3, T2_FD_MRC = 4 };
+enum { T2_STATS = 0, T2_PD = 1, T2_FD = 2 };
 
 // Geometry of one launch (host-computed).
 struct Tc2Geom {
   int K;        // antennas per unit
   int nchunk;   // stages per group = ceil(K / 32)
-  int upi;      // units per item (1: PD / summed statistics; C: per cluster)
-  int gc, gn;   // a group = gn items x gc clusters (gc * gn = 4)
+  int upi;      // units per item (1: PD / summed statistics; C: per cluster) = groups per item block
   int us;       // complex entries per H row (u_stride, even, <= 16)
   int T;
   int NS;       // stage ring depth
   int stage_bytes;
   int hbytes;   // bytes of the H box (4 units x 32 x 2us floats)
-  int ybox;     // bytes of one Y box (gn items x T rows x 68 floats)
-  int ystride;  // shared-memory stride between the Y boxes (128-byte aligned)
-  int lean;     // compact solver work areas: 1 = t2_solve_pair / statistics, 2 = MRC
-  int64_t U_tot;  // units in the launch
-  int64_t G_tot;  // groups in the launch
+  int ybox;     // bytes of the Y box (4 items x T rows x 68 floats)
+  int lean;     // compact solver work areas (G, y_mrc, pivot columns, flags)
+  int64_t n_items;
+  int64_t G_tot;  // groups in the launch = ceil(n_items / 4) * upi
 };
 
 struct Tc2Layout {
-  int bars, tmem_slot, fdc, stg, work, work_stride, total;
+  int bars, tmem_slot, stg, work, work_stride, fdacc, fdacc_stride, total;
   WorkLayout w;
 };
+
+// FD fusion sums of one solver warp (T2FdAcc): num [2][T][16] float2, den /
+// harm [2][16], wb [C][16], status
+__host__ __device__ inline int t2_fdacc_bytes(int T, int C) {
+  return align_up(2 * T * 16 * 8 + 2 * 2 * 16 * 4 + C * 16 * 4 + 16, 128);
+}
 
 __host__ __device__ inline Tc2Layout make_tc2_layout(const Tc2Geom& g, int TP, int C, bool fd) {
   Tc2Layout L;
@@ -117,43 +121,48 @@ __host__ __device__ inline Tc2Layout make_tc2_layout(const Tc2Geom& g, int TP, i
   o += (3 * g.NS + 4) * 8;
   L.tmem_slot = o;
   o += 16;
-  L.fdc = o;
-  o += fd ? T2_FD_CNT * 4 : 0;
   o = align_up(o, 1024);
   L.stg = o;
   o += g.NS * g.stage_bytes;
   L.work = o;
-  L.w = make_work_layout(0, 16, TP, C, false, fd);
-  if (g.lean) {  // only what the kernel's epilogue touches (smem for the stage ring)
+  L.w = make_work_layout(0, 16, TP, C, false, false);
+  {  // compact work area: G, y_mrc, the pivot-column buffers, status flags
     const int LD = 16 + 2;
     int q = 0;
     L.w.G = q;
     q += 16 * LD * 8;
     L.w.Z = q;
     q += TP * LD * 8;
-    L.w.Sv = L.w.Vv = L.w.Fb = L.w.gb = L.w.num = L.w.phi = L.w.coef = L.w.den = L.w.harm = L.w.wbuf = L.w.Z;
-    if (g.lean == 2) {  // MRC team epilogue: estimates, variances, gains
-      L.w.X = q;
-      q += TP * LD * 8;
-      L.w.s2 = q;
-      q += 16 * 4;
-      L.w.gn = q;
-      q += 16 * 4;
-      L.w.dg = q;
-      q += 16 * 4;
-      L.w.W = L.w.Z;
-    } else {  // t2_solve_pair / statistics: the pivot-column buffers
-      L.w.W = q;
-      q += 32 * 8;
-      L.w.X = L.w.s2 = L.w.gn = L.w.dg = L.w.Z;
-    }
+    L.w.W = q;
+    q += 32 * 8;
     L.w.flags = q;
+    L.w.X = L.w.Sv = L.w.Vv = L.w.Fb = L.w.gb = L.w.num = L.w.Z;
+    L.w.phi = L.w.coef = L.w.s2 = L.w.gn = L.w.dg = L.w.den = L.w.harm = L.w.wbuf = L.w.Z;
     L.w.total = align_up(q + 16, 128);
   }
   L.work_stride = L.w.total;
   o += T2_NWORK * L.work_stride;
+  L.fdacc = o;
+  L.fdacc_stride = fd ? t2_fdacc_bytes(g.T, C) : 0;
+  o += T2_NSOLV * L.fdacc_stride;
   L.total = align_up(o, 128);
   return L;
+}
+
+// Stream order of a CTA's groups: item blocks go in pairs (2 bp, 2 bp + 1)
+// whose groups alternate, (block 2bp, cluster 0), (2bp + 1, 0), (2bp, 1), ...,
+// so consecutive groups alternate the two accumulators and both solver sets
+// (set s reads the blocks of parity s) stay busy; an unpaired last block runs
+// its clusters in order.
+__device__ __forceinline__ void t2_group(int gl, int upi, int nblocks, int& lb, int& c) {
+  const int bp = gl / (2 * upi), r = gl - bp * 2 * upi;
+  if (2 * bp + 1 < nblocks) {
+    lb = 2 * bp + (r & 1);
+    c = r >> 1;
+  } else {
+    lb = 2 * bp;
+    c = r;
+  }
 }
 
 // ---- PTX wrappers ------------------------------------------------------------
@@ -172,11 +181,6 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "{%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "l"(policy)
       : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
-               : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0),
@@ -281,9 +285,19 @@ __device__ __forceinline__ int t2_slice(float2 z, const ConstParams& cp) {
   return i * cp.L + j;
 }
 
-// Two units per warp, one per half-warp (ZF / L-MMSE, equalize.py:153-172 +
-// unbiased_output :179-195).  Lane (h = lane / 16, j = lane % 16) owns column
-// j of unit h's matrix M = G + rho I (all 16 rows in registers).  In-place
+// FD fusion sums of one warp's item (fusion.py:108-124), accumulated in
+// shared memory per half-warp in cluster order; combined at the item's end.
+struct T2FdAcc {
+  float2* num;  // [2][TP][16]  sum_c w_c z_c
+  float* den;   // [2][16]      sum_c w_c
+  float* harm;  // [2][16]      sum_c 1 / max(sigma2_c, floor)
+  float* wb;    // [C][16]      w_c (for nu)
+  int* st;      // status of the item (first failing cluster's code)
+};
+
+// Two units per warp, one per half-warp: MRC / ZF / L-MMSE (equalize.py:130-
+// 195).  Lane (h = lane / 16, j = lane % 16) owns column j of unit h's matrix
+// M = G + rho I (all 16 rows in registers).  ZF / L-MMSE: in-place
 // Gauss-Jordan inverse without pivoting (M is Hermitian positive definite),
 // written as the branch-free rank-1 update  m_ij -= c_i r_j  with
 //   c_i = M_ik (i != k), c_k = p - 1;   r_j = M_kj / p (j != k), r_k = 1 + 1/p
@@ -292,16 +306,18 @@ __device__ __forceinline__ int t2_slice(float2 z, const ConstParams& cp) {
 // by lane k through a double-buffered shared-memory column and read back as
 // broadcasts.  A = M^-1 is Hermitian, so lane j also holds row j of A
 // (conjugated): x_t[j] = sum_i conj(A_ij) y_t[i], sigma2 = N0 A_jj,
-// c = 1 - rho A_jj, unbiased z / c and N0 A_jj / c.  Outputs go straight to
-// x-hat / decisions / sigma2 / status (PD) or to the cluster's fold record
-// (FD).  A pivot below 8 u eps of its original diagonal is SingularGramError
-// (the fp32 counterpart of zpotrf's "not positive definite").
+// c = 1 - rho A_jj, unbiased z / c and N0 A_jj / c.  MRC: d = G_jj, z = y / d,
+// sigma2 = N0/d + Es sum_{v != j} |G_jv|^2 / d^2.  A pivot below 8 u eps of
+// its original diagonal is SingularGramError (the fp32 counterpart of
+// zpotrf's "not positive definite").  PD writes x-hat / decisions / sigma2 /
+// gain / status; FD adds w z, w, 1/sigma2 (w = 1/max(sigma2, 1e-15), MRC: the
+// Gram diagonal, fusion.py:96-105,149-151) to the half-warp's sums in `acc`.
 template <bool FD>
 __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
-                              const bool* valid, int lane) {
+                              const bool* valid, int lane, const T2FdAcc* acc = nullptr) {
   const int h = lane >> 4, j = lane & 15;
   const int u = p.u, T = p.T, LD = w[0].LD;
-  const bool lmmse = p.kind == EQ_LMMSE;
+  const bool lmmse = p.kind == EQ_LMMSE, mrc = p.kind == EQ_MRC;
   const bool act = h ? valid[1] : valid[0];
   const int64_t nh = h ? n[1] : n[0];
   const int ch = h ? c[1] : c[0];
@@ -325,92 +341,124 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
     }
     m[i] = v;
   }
-  const float tolf = 8.f * (float)u * FLT_EPSILON;
   bool bad = false;
-  // Rotating register order: at step k the lane's row-k element is m[k % 4]
-  // of the current frame, and after every 4 steps the registers rotate by 4,
-  // so all indices stay static with a 4-step unrolled body; the pivot column
-  // is published and read in the same frame.  Padded steps (k >= u) are
-  // identity pivots and no-ops, but are kept so that the frame returns to
-  // the original order after 16 steps.
+  if (!mrc) {
+    const float tolf = 8.f * (float)u * FLT_EPSILON;
+    // Rotating register order: at step k the lane's row-k element is m[k % 4]
+    // of the current frame, and after every 4 steps the registers rotate by
+    // 4, so all indices stay static with a 4-step unrolled body; the pivot
+    // column is published and read in the same frame.  Padded steps (k >= u)
+    // are identity pivots and no-ops: whole groups of 4 of them are skipped
+    // and replaced by the bare register rotation that restores the frame.
 #pragma unroll 1
-  for (int k0 = 0; k0 < 16; k0 += 4) {
+    for (int k0 = 0; k0 < 16; k0 += 4) {
+      if (k0 >= u) {
+        float2 t4[4];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int k = k0 + kk;
-      float2* cb = colb + (kk & 1) * 16;
-      if (j == k) {  // publish the pivot column (a failed pivot is replaced by 1)
-        float2 pk = m[kk];
-        if (act && k < u && !(pk.x > tolf * dg)) {
-          bad = true;
-          pk = make_float2(1.f, 0.f);
+        for (int i = 0; i < 4; ++i) t4[i] = m[i];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
+        continue;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = k0 + kk;
+        float2* cb = colb + (kk & 1) * 16;
+        if (j == k) {  // publish the pivot column (a failed pivot is replaced by 1)
+          float2 pk = m[kk];
+          if (act && k < u && !(pk.x > tolf * dg)) {
+            bad = true;
+            pk = make_float2(1.f, 0.f);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float2 a0 = (i == kk) ? pk : m[i], a1 = (i + 1 == kk) ? pk : m[i + 1];
+            *reinterpret_cast<float4*>(cb + i) = make_float4(a0.x, a0.y, a1.x, a1.y);
+          }
         }
+        __syncwarp();
+        float2 cc[16];
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
-          const float2 a0 = (i == kk) ? pk : m[i], a1 = (i + 1 == kk) ? pk : m[i + 1];
-          *reinterpret_cast<float4*>(cb + i) = make_float4(a0.x, a0.y, a1.x, a1.y);
+          const float4 v = *reinterpret_cast<const float4*>(cb + i);
+          cc[i] = make_float2(v.x, v.y);
+          cc[i + 1] = make_float2(v.z, v.w);
         }
-      }
-      __syncwarp();
-      float2 cc[16];
+        const float pv = cc[kk].x;
+        const float rp = __frcp_rn(pv);
+        const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[kk], rp);
+        cc[kk] = make_float2(pv - 1.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        const float4 v = *reinterpret_cast<const float4*>(cb + i);
-        cc[i] = make_float2(v.x, v.y);
-        cc[i + 1] = make_float2(v.z, v.w);
+        for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
       }
-      const float pv = cc[kk].x;
-      const float rp = __frcp_rn(pv);
-      const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[kk], rp);
-      cc[kk] = make_float2(pv - 1.f, 0.f);
+      float2 t4[4];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
+      for (int i = 0; i < 4; ++i) t4[i] = m[i];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
     }
-    float2 t4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) t4[i] = m[i];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
   }
-  const unsigned bm = __ballot_sync(0xffffffffu, bad);
-  float ajj = 0.f;
+  // per-lane scalars: A_jj (ZF / L-MMSE) or d = G_jj and the off-diagonal
+  // row energy (MRC; row j = conj(column j))
+  float ajj = 0.f, off = 0.f;
 #pragma unroll
-  for (int i = 0; i < 16; ++i)
+  for (int i = 0; i < 16; ++i) {
     if (i == j) ajj = m[i].x;
+    else if (mrc && i < u) off += c_abs2(m[i]);
+  }
+  if (mrc && act && j < u && !(ajj > 0.f)) bad = true;  // MRC: Gram diagonal <= 0
   const bool unb = lmmse && (FD || p.unbias);
   const float cgain = 1.f - rho * ajj;
-  const float sc = unb ? __frcp_rn(cgain) : 1.f;
+  const float sc = mrc ? __frcp_rn(ajj) : unb ? __frcp_rn(cgain) : 1.f;
   const bool badc = act && j < u && unb && !(cgain > 0.f);
-  const unsigned bc = __ballot_sync(0xffffffffu, badc);
-  const int st = (((bm | bc) >> (16 * h)) & 0xffffu) ? ST_SINGULAR : ST_OK;
-  float* rec = nullptr;
-  if constexpr (FD) rec = p.fd_scratch + ((size_t)nh * p.C + ch) * fd_record_floats(u, T, u);
+  const unsigned bm = __ballot_sync(0xffffffffu, bad || badc);
+  int st = ((bm >> (16 * h)) & 0xffffu) ? ST_SINGULAR : ST_OK;
+  float s2 = 0.f;
+  if (mrc) {
+    const float rd = __frcp_rn(ajj);
+    s2 = n0h * rd + p.es * off * rd * rd;
+  } else {
+    const float nv = n0h * ajj;
+    s2 = (p.kind == EQ_ZF) ? nv : (unb ? nv / cgain : nv);
+  }
+  // FD weight of this cluster for UE j (fusion.py:96-105,149-151)
+  const float inv = 1.f / fmaxf(s2, VAR_FLOOR);
+  const float wgt = mrc ? ajj : inv;
+  if (FD && !mrc && act && j < u && !(s2 > 0.f)) st = ST_BADVAR;  // optimal_fusion_weights rejects sigma2 <= 0
+  const int hb = FD ? h * 16 : 0;
   if (act && j < u) {
     for (int t = 0; t < T; t += 2) {  // symbols t, t + 1: four independent chains
       const int t1 = (t + 1 < T) ? t + 1 : t;
       const float2* z0 = Z + t * LD;
       const float2* z1 = Z + t1 * LD;
       float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+      if (mrc) {
+        a0 = z0[j];
+        b0 = z1[j];
+      } else {
 #pragma unroll
-      for (int i0 = 0; i0 < 16; i0 += 8) {  // half a row of loads in flight at a time
-        if (i0 >= u) break;
-        float4 y0[4], y1[4];
+        for (int i0 = 0; i0 < 16; i0 += 8) {  // half a row of loads in flight at a time
+          if (i0 >= u) break;
+          float4 y0[4], y1[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = i0 + 2 * e;
-          y0[e] = (i < u) ? *reinterpret_cast<const float4*>(z0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-          y1[e] = (i < u) ? *reinterpret_cast<const float4*>(z1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+          for (int e = 0; e < 4; ++e) {
+            const int i = i0 + 2 * e;
+            y0[e] = (i < u) ? *reinterpret_cast<const float4*>(z0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            y1[e] = (i < u) ? *reinterpret_cast<const float4*>(z1 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = i0 + 2 * e;
-          // y_t[i] beyond u was never written (zeroed above; its A column is zero)
-          c_fma_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
-          c_fma_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
-          c_fma_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
-          c_fma_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+          for (int e = 0; e < 4; ++e) {
+            const int i = i0 + 2 * e;
+            // y_t[i] beyond u is zero (the recombination zeroes it; its A column is zero)
+            c_fma_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
+            c_fma_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
+            c_fma_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
+            c_fma_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+          }
         }
       }
 #pragma unroll
@@ -419,7 +467,8 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
         const int te = t + e;
         const float2 x = c_scale(e ? c_add(b0, b1) : c_add(a0, a1), sc);
         if constexpr (FD) {
-          reinterpret_cast<float2*>(rec)[te * u + j] = x;
+          float2& sum = acc->num[(h * T + te) * 16 + j];
+          sum = c_add(sum, c_scale(x, wgt));
         } else {
           const size_t o = ((size_t)nh * T + te) * u + j;
           p.xhat[o] = x;
@@ -427,24 +476,67 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
         }
       }
     }
-    const float nv = n0h * ajj;
-    const float s2 = (p.kind == EQ_ZF) ? nv : (unb ? nv / cgain : nv);
     if constexpr (FD) {
-      rec[2 * T * u + j] = s2;
+      acc->den[hb + j] += wgt;
+      acc->harm[hb + j] += inv;
+      acc->wb[ch * 16 + j] = wgt;
     } else {
       p.sigma2[(size_t)nh * u + j] = s2;
-      if (p.gain && lmmse) p.gain[(size_t)nh * u + j] = cgain;
+      if (p.gain && (lmmse || mrc)) p.gain[(size_t)nh * u + j] = mrc ? ajj : cgain;
     }
   }
-  if (act && j == 0) {
-    if constexpr (FD) {
-      int* f = reinterpret_cast<int*>(rec + 2 * T * u + 2 * u);
-      f[0] = st;
-      f[1] = 0x7fffffff;
-    } else {
-      p.status[nh] = st;
-      if (p.iters) p.iters[nh] = 0;
+  if constexpr (FD) {
+    // the first failing cluster's code (half 0 holds the earlier cluster)
+    const unsigned bv = __ballot_sync(0xffffffffu, act && j < u && st == ST_BADVAR);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int code = ((bm >> (16 * hh)) & 0xffffu) ? ST_SINGULAR : ((bv >> (16 * hh)) & 0xffffu) ? ST_BADVAR : 0;
+      if (lane == 0 && code) atomicCAS(acc->st, 0, code);
     }
+  } else if (act && j == 0) {
+    p.status[nh] = st;
+    if (p.iters) p.iters[nh] = 0;
+  }
+}
+
+// The item's FD fusion (fusion.py:108-124, 141-154) from the two half-warps'
+// sums: x = sum_c w_c z_c / sum_c w_c, sigma2 = 1 / sum_c 1/max(sigma2_c,
+// 1e-15), nu_c = w_c / sum w; or the raw sums for a cross-GPU reduction
+// (ARCH_FD_PARTIAL: fd_acc [n][2Tu + 2u], fd_wraw [n][C][u]).
+__device__ inline void t2_fd_finish(const T2FdAcc& acc, const EqParams& p, int64_t n, int lane) {
+  const int u = p.u, T = p.T, C = p.C;
+  const int h = lane >> 4, j = lane & 15;
+  const int st = *acc.st;
+  if (j < u) {
+    const float den = acc.den[j] + acc.den[16 + j], harm = acc.harm[j] + acc.harm[16 + j];
+    if (p.arch == ARCH_FD) {
+      const float rden = 1.f / den;
+      for (int t = h; t < T; t += 2) {
+        const float2 x = c_scale(c_add(acc.num[t * 16 + j], acc.num[(T + t) * 16 + j]), rden);
+        const size_t o = ((size_t)n * T + t) * u + j;
+        p.xhat[o] = x;
+        if (p.dec) p.dec[o] = (uint8_t)t2_slice(x, p.cp);
+      }
+      if (h == 0) p.sigma2[(size_t)n * u + j] = 1.f / harm;
+      if (p.nu)
+        for (int c = h; c < C; c += 2) p.nu[((size_t)n * C + c) * u + j] = acc.wb[c * 16 + j] * rden;
+    } else {
+      float* dst = p.fd_acc + (size_t)n * (2 * T * u + 2 * u);
+      for (int t = h; t < T; t += 2) {
+        const float2 v = c_add(acc.num[t * 16 + j], acc.num[(T + t) * 16 + j]);
+        dst[2 * (t * u + j)] = v.x;
+        dst[2 * (t * u + j) + 1] = v.y;
+      }
+      if (h == 0) {
+        dst[2 * T * u + j] = den;
+        dst[2 * T * u + u + j] = harm;
+      }
+      for (int c = h; c < C; c += 2) p.fd_wraw[((size_t)n * C + c) * u + j] = acc.wb[c * 16 + j];
+    }
+  }
+  if (lane == 0) {
+    p.status[n] = st;
+    if (p.iters) p.iters[n] = 0;
   }
 }
 
@@ -509,8 +601,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     tc2_kernel(const __grid_constant__ EqParams p, const __grid_constant__ CUtensorMap hmap,
                const __grid_constant__ CUtensorMap ymap, const __grid_constant__ Tc2Geom g) {
   extern __shared__ __align__(1024) char smem[];
-  constexpr bool fd = (MODE == T2_FD || MODE == T2_FD_MRC);
-  constexpr bool mrc = (MODE == T2_PD_MRC || MODE == T2_FD_MRC);
+  constexpr bool fd = (MODE == T2_FD);
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int NS = g.NS;
   const Tc2Layout L = make_tc2_layout(g, p.TP, p.C, fd);
@@ -520,7 +611,6 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
   uint64_t* acc_full = stage_empty + NS;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
-  int* fd_count = reinterpret_cast<int*>(smem + L.fdc);
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&raw_full[s], 1);
@@ -533,8 +623,6 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     }
     fence_mbar_init();
   }
-  if (fd)
-    for (int k = tid; k < T2_FD_CNT; k += blockDim.x) fd_count[k] = 0;
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -545,14 +633,15 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
   const long long t_start = clock64();
 #endif
 
-  // contiguous range of whole items per CTA: blocks of gpi = max(1, upi / 4)
-  // groups (groups never straddle items: upi | 4 or 4 | upi), so all clusters
-  // of an item meet at one CTA's FD arrival counter
-  const int gpi = g.upi > 4 ? g.upi / 4 : 1;
-  const int64_t nblk = g.G_tot / gpi;
+  // Groups are item-major: group g = (item block b = g / upi, cluster
+  // c = g % upi) holds cluster c of items 4b .. 4b + 3 (unit q = item 4b + q),
+  // so a solver warp's lane quarter sees every cluster of one item and can
+  // fuse them (FD) without leaving the warp.  A CTA owns whole item blocks.
+  const int64_t nblk = g.G_tot / g.upi;
   const int64_t per_cta = nblk / gridDim.x, extra = nblk % gridDim.x;
-  const int64_t g_first = (blockIdx.x * per_cta + min((int64_t)blockIdx.x, extra)) * gpi;
-  const int ngroups = (int)(per_cta + (blockIdx.x < extra ? 1 : 0)) * gpi;
+  const int64_t b_first = blockIdx.x * per_cta + min((int64_t)blockIdx.x, extra);
+  const int nblocks = (int)(per_cta + (blockIdx.x < extra ? 1 : 0));
+  const int ngroups = nblocks * g.upi;
   const int nch = g.nchunk;
   const uint32_t stg0 = smem_u32(smem + L.stg);
 
@@ -564,34 +653,31 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       const uint64_t policy = l2_evict_first_policy();
       const int total = ngroups * nch;
       // stage sequence number -> (group, chunk) coordinates
-      auto coords = [&](int sq, int& j, int64_t& u0, int& n0, int& c0) {
+      auto coords = [&](int sq, int& j, int& item0, int& c0) {
         const int gl = sq / nch;
         j = sq - gl * nch;
-        u0 = (g_first + gl) * 4;
-        n0 = (int)(u0 / g.upi);
-        c0 = (int)(u0 % g.upi);
+        int lb;
+        t2_group(gl, g.upi, nblocks, lb, c0);
+        item0 = (int)((b_first + lb) * 4);
       };
       auto prefetch = [&](int sq) {
-        int j, n0, c0;
-        int64_t u0;
-        coords(sq, j, u0, n0, c0);
-        tma_prefetch_3d(&hmap, 0, 32 * j, (int)u0);
-        for (int cl = 0; cl < g.gc; ++cl) tma_prefetch_4d(&ymap, 64 * j, c0 + cl, 0, n0);
+        int j, item0, c0;
+        coords(sq, j, item0, c0);
+        tma_prefetch_4d(&hmap, 0, 32 * j, c0, item0);
+        tma_prefetch_4d(&ymap, 64 * j, c0, 0, item0);
       };
       for (int sq = NS; sq < 2 * NS && sq < total; ++sq) prefetch(sq);
       int s = 0;
       uint32_t ph = 0;
       for (int sq = 0; sq < total; ++sq) {
         if (sq >= NS) T2_WAIT(&stage_empty[s], ph ^ 1u, 1);
-        int j, n0, c0;
-        int64_t u0;
-        coords(sq, j, u0, n0, c0);
+        int j, item0, c0;
+        coords(sq, j, item0, c0);
         const uint32_t bar = smem_u32(&raw_full[s]);
-        mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(g.hbytes + g.gc * g.ybox));
+        mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(g.hbytes + g.ybox));
         const uint32_t dst = stg0 + (uint32_t)(s * g.stage_bytes);
-        tma_load_3d(dst, &hmap, 0, 32 * j, (int)u0, bar, policy);
-        for (int cl = 0; cl < g.gc; ++cl)
-          tma_load_4d(dst + g.hbytes + cl * g.ystride, &ymap, 64 * j, c0 + cl, 0, n0, bar, policy);
+        tma_load_4d(dst, &hmap, 0, 32 * j, c0, item0, bar, policy);
+        tma_load_4d(dst + g.hbytes, &ymap, 64 * j, c0, 0, item0, bar, policy);
         if (sq + 2 * NS < total) prefetch(sq + 2 * NS);  // keep 2 NS stages of lookahead in L2
         if (++s == NS) {
           s = 0;
@@ -610,9 +696,13 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       constexpr int PB[6] = {0, 1, 0, 1, 2, 0};
       int s = 0;
       uint32_t ph = 0;
+      int uses[2] = {0, 0};  // groups written into each accumulator so far
       for (int gl = 0; gl < ngroups; ++gl) {
-        const int a = gl & 1;
-        if (gl >= 2) T2_WAIT(&acc_empty[a], (uint32_t)(((gl >> 1) - 1) & 1), 2);
+        int lb, cg;
+        t2_group(gl, g.upi, nblocks, lb, cg);
+        const int a = lb & 1;  // item blocks alternate accumulators
+        if (uses[a] >= 1) T2_WAIT(&acc_empty[a], (uint32_t)((uses[a] - 1) & 1), 2);
+        ++uses[a];
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(256 * a);
         for (int j = 0; j < nch; ++j) {
@@ -672,9 +762,8 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       const int kp = (e & 3) + 4 * ((e >> 3) & 3);
       const int tb = ((e >> 2) & 1) + 2 * ((e >> 5) & 1);
       const int q = e >> 6;
-      const int nl = q / g.gc, cl = q - nl * g.gc;
       yt0[i] = 4 * tb;
-      yld[i] = (g.hbytes >> 2) + cl * (g.ystride >> 2) + (nl * T + 4 * tb) * T2_YROW + 4 * kp;
+      yld[i] = (g.hbytes >> 2) + (q * T + 4 * tb) * T2_YROW + 4 * kp;
       yst0[i] = t2_off(2 + (q >> 1), 2 * kp, 32 * (q & 1) + 8 * tb);
       yst1[i] = yst0[i] + 128 + (((yst0[i] >> 4) & 1) ? -16 : 16);
     }
@@ -746,6 +835,9 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     }
   } else {
     // ----------------------------------------------------------- solvers ----
+    // set s = 0, 1 owns accumulator s, i.e. the item blocks of parity s; warp
+    // (s, q) handles item 4b + q of each of its blocks, reading the units of
+    // its lane quarter in order, two per pass (one per half-warp)
     const int sv = warp - T2_FIRST_SOLV;
     const int sset = sv >> 2;  // = the accumulator this warp reads
     const int q = warp & 3;    // TMEM lane quarter this warp may access
@@ -760,29 +852,49 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       wl.dg += base; wl.den += base; wl.harm += base; wl.wbuf += base; wl.flags += base;
       w[k] = make_work(smem, wl, 16);
     }
-    const int u = p.u, T = p.T, LD = w[0].LD;
+    const int u = p.u, T = p.T, LD = w[0].LD, upi = g.upi;
     const int uh = lane >> 1, s_im = lane & 1;  // this lane's H feature: UE uh, re/im
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
     int cl_first = 1;
-    for (int gl = sset; gl < ngroups; gl += 4) {
+    T2FdAcc acc;
+    if constexpr (fd) {
+      char* ab = smem + L.fdacc + sv * L.fdacc_stride;
+      acc.num = reinterpret_cast<float2*>(ab);
+      acc.den = reinterpret_cast<float*>(ab + 2 * T * 16 * 8);
+      acc.harm = acc.den + 32;
+      acc.wb = acc.harm + 32;
+      acc.st = reinterpret_cast<int*>(acc.wb + upi * 16);
+    }
+    // this warp's unit sequence: (block lb, cluster c), lb = sset, sset + 2, ...
+    const int units = ((nblocks - sset + 1) / 2) * upi;
+    int use = 0;  // reads of accumulator sset so far (mbarrier phase)
+    for (int k0 = 0; k0 < units; k0 += 2) {
       int64_t n[2];
       int c[2];
       float n0[2];
       bool valid[2];
+      int lbk[2];
+      int cnt = 0;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {  // groups gl, gl + 2 (accumulator sset)
+      for (int k = 0; k < 2; ++k) {
         valid[k] = false;
         n[k] = 0;
         c[k] = 0;
         n0[k] = 0.f;
-        const int gg = gl + 2 * k;
-        if (gg >= ngroups) continue;
-        const int64_t uid = (g_first + gg) * 4 + q;
-        valid[k] = uid < g.U_tot;
-        n[k] = uid / g.upi;
-        c[k] = (int)(uid - n[k] * g.upi);
+        lbk[k] = -1;
+        const int uix = k0 + k;
+        if (uix >= units) continue;
+        const int lb = sset + 2 * (uix / upi);
+        const int cc = uix - (uix / upi) * upi;
+        if (fd && k == 1 && cc == 0) continue;  // FD pairs stay inside one item block
+        ++cnt;
+        lbk[k] = lb;
+        c[k] = cc;
+        n[k] = (b_first + lb) * 4 + q;
+        valid[k] = n[k] < g.n_items;
         if (valid[k] && MODE != T2_STATS) n0[k] = item_n0(p, n[k]);  // global load before the wait
-        T2_WAIT(&acc_full[sset], (uint32_t)((gg >> 1) & 1), 1);
+        T2_WAIT(&acc_full[sset], (uint32_t)(use & 1), 1);
+        ++use;
         tc_fence_after();
         uint32_t gr[32], yr[32];
         tmem_ld32_nw(tq + (uint32_t)(256 * sset + 32 * q), gr);
@@ -813,57 +925,28 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
         }
         reset_flags(w[k], tm);
       }
+      k0 -= 2 - cnt;  // a unit not taken (FD block boundary) is read in the next pass
       __syncwarp();
-      if (!valid[0] && !valid[1]) continue;
       if constexpr (MODE == T2_STATS) {
 #pragma unroll
         for (int k = 0; k < 2; ++k)
           if (valid[k]) unit_epilogue<16, Team<32, -1>, 0>(w[k], p, n[k], c[k], true, cl_first, tm, nullptr, 0.f);
         continue;
-      }
-      if constexpr (mrc) {
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          if (!valid[k]) continue;
-          if constexpr (MODE == T2_PD_MRC) {
-            unit_epilogue<16, Team<32, -1>, 1>(w[k], p, n[k], 0, true, cl_first, tm, nullptr, n0[k]);
-          } else {
-            EpiArgs ea;
-            ea.kind = p.kind;
-            ea.u = u;
-            ea.T = T;
-            ea.n0 = n0[k];
-            ea.es = p.es;
-            ea.damping = p.damping;
-            ea.t_max = p.t_max;
-            ea.beta = p.cl_beta[c[k]];
-            ea.lama_scale = p.cl_scale[c[k]];
-            ea.unbias = true;
-            ea.ablate = 0;
-            linear_unit<16>(w[k], ea, tm);
-            fd_stash(w[k], p, n[k], c[k], tm);
-          }
-        }
+      } else if constexpr (MODE == T2_PD) {
+        t2_solve_pair<false>(w, p, n, c, n0, valid, lane);
       } else {
-        t2_solve_pair<MODE == T2_FD>(w, p, n, c, n0, valid, lane);
-      }
-      if constexpr (fd) {
-        // count the arrivals; the last of an item's C clusters folds the
-        // records in cluster order (fusion.py:141-154); Z is free scratch now
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          if (!valid[k]) continue;
-          __threadfence_block();
+        const bool item_ok = lbk[0] >= 0 && (b_first + lbk[0]) * 4 + q < g.n_items;
+        if (c[0] == 0 && lbk[0] >= 0) {  // a new item: clear its fusion sums
+          for (int e = lane; e < 2 * T * 16; e += 32) acc.num[e] = make_float2(0.f, 0.f);
+          acc.den[lane] = 0.f;
+          acc.harm[lane] = 0.f;
+          if (lane == 0) *acc.st = 0;
           __syncwarp();
-          int last = 0;
-          if (lane == 0) last = (atomicAdd(&fd_count[n[k] & (T2_FD_CNT - 1)], 1) == p.C - 1);
-          last = __shfl_sync(0xffffffffu, last, 0);
-          if (last) {
-            if (lane == 0) fd_count[n[k] & (T2_FD_CNT - 1)] = 0;
-            __threadfence_block();
-            fd_finish(reinterpret_cast<float*>(w[k].Z), p, n[k], tm);
-          }
         }
+        t2_solve_pair<true>(w, p, n, c, n0, valid, lane, &acc);
+        __syncwarp();
+        const int clast = (lbk[1] >= 0) ? c[1] : c[0];
+        if (item_ok && clast == upi - 1) t2_fd_finish(acc, p, n[0], lane);
       }
       __syncwarp();
     }
