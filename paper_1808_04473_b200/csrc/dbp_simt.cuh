@@ -215,10 +215,6 @@ __device__ __forceinline__ void reduce_tiles(float2 (&acc)[4][4], const TileInfo
         }
       }
   }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
   __syncthreads();
 }
 
@@ -310,6 +306,12 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
     if (!unit_end) continue;
     reduce_tiles<UP, NT>(acc, ti, red, w, p.T, ntiles);
     if (!(p.ablate & 1)) unit_epilogue<UP, Team<NT, 0>, CLS>(w, p, n, cd.cluster, item_end, cl_first, tm);
+    // the accumulators restart after the epilogue (not before it: zeroed
+    // registers kept live across the epilogue made the LAMA instantiation spill)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
     __syncthreads();
   }
 }
