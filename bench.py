@@ -352,6 +352,11 @@ def main():
     if world > 1 or args.dist:
         from paper_1808_04473_b200 import distributed
 
+        if world == 1:  # --dist without torchrun: a 1-rank group
+            for k, v in (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1"),
+                         ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
+                os.environ.setdefault(k, v)
+
         return distributed.bench_main(args, wl, args.config, sys.modules[__name__])
     return single_gpu(args, wl, args.config)
 

@@ -219,6 +219,33 @@ def lama_equalize(g, y_mrc, symbols, es, n0, beta, t_max=10, damping=1.0,
     return z, np.full(u, tau), trace
 
 
+def lama_receive_domain(y, h, symbols, n0, beta, t_max):
+    """The receive-domain message passing the Gram-domain recursion is
+    derived from -- the reference's independent check of lama_equalize
+    (tests/oracles.py:55-82, used by test_acceptance.py:99-113):
+        z^t = s^t + H^H r^t,   eff^t = N0 (1 + tau^t)
+        (F, G) = posterior(z^t, eff^t),  tau^{t+1} = beta/N0 mean(G)
+        r^{t+1} = y - H F + tau^{t+1} / (1 + tau^t) r^t,  s^{t+1} = F
+    from s^1 = E[S], tau^1 = beta Var[S] / N0, r^1 = y - H s^1.  Returns the
+    list of (z^t, phi^t = N0 tau^t / beta)."""
+    y = np.asarray(y, dtype=np.complex128)
+    h = np.asarray(h, dtype=np.complex128)
+    symbols = np.asarray(symbols, dtype=np.complex128)
+    mean = symbols.mean()
+    s = np.full(h.shape[1], mean, dtype=np.complex128)
+    tau = beta * float(np.mean(np.abs(symbols - mean) ** 2)) / n0
+    r = y - h @ s
+    out = []
+    for _ in range(t_max):
+        z = s + h.conj().T @ r
+        out.append((z, n0 * tau / beta))
+        f, g = posterior_mean_var(z, n0 * (1.0 + tau), symbols)
+        tau_next = beta / n0 * float(np.mean(g))
+        r = y - h @ f + (tau_next / (1.0 + tau)) * r
+        s, tau = f, tau_next
+    return out
+
+
 def hard_detect_index(z, symbols):
     """equalize.py:262-268: argmin_k |z - a_k|^2, ties to the lowest k
     (np.argmin returns the first minimum).  Returned as indices."""

@@ -560,8 +560,8 @@ __global__ void __launch_bounds__(32 * T2S_WARPS) t2_stats_solve_kernel(const __
     char* base = smem + (2 * warp + k) * work_stride;
     w[k].G = reinterpret_cast<float2*>(base);
     w[k].Z = reinterpret_cast<float2*>(base + 16 * LD * 8);
-    w[k].W = reinterpret_cast<float2*>(base + 32 * LD * 8);
-    w[k].flags = reinterpret_cast<int*>(base + 32 * LD * 8 + 32 * 8);
+    w[k].W = reinterpret_cast<float2*>(base + (16 + p.TP) * LD * 8);  // layout of launch_t2_stats_solve
+    w[k].flags = reinterpret_cast<int*>(base + (16 + p.TP) * LD * 8 + 32 * 8);
     w[k].X = w[k].Z;
     w[k].LD = LD;
   }

@@ -112,3 +112,27 @@ def test_tc2_statistics(n, b, c, u, t, summed):
             # core's fp32 accumulator over up to 256 antennas
             assert np.abs(o[i, k, :u * u].reshape(u, u) - G).max() < 1e-5 * np.abs(G).max(), (i, k, "G")
             assert np.abs(o[i, k, u * u:].reshape(t, u) - Z).max() < 1e-5 * np.abs(Z).max(), (i, k, "Z")
+
+
+@pytest.mark.parametrize("t", [None, 1, 3, 16])
+@pytest.mark.parametrize("kind", ["zf", "lmmse"])
+def test_stats_solve_symbol_counts(kind, t):
+    """linear_equalize on fused statistics (the warp-pair solver of
+    t2_stats_solve_kernel, whose work areas are sized by T): one receive
+    vector per channel (t None) and T = 1 / 3 / 16, odd item count."""
+    n, b, u = 9, 64, 16
+    H, Y, const, n0 = _inputs(n, b, u, t or 1, 4, 7 + (t or 0))
+    if t is None:
+        Y = Y[:, 0]
+    stats = dbp.centralized_stats(H, Y)
+    assert _lib.lib().dbp_last_kernel() == _lib.KERNEL_TC_BF16
+    out = dbp.linear_equalize(kind, stats, n0)
+    Ys = Y if t is not None else Y[:, None]
+    for i in range(n):
+        zi = np.asarray(out.z[i]).reshape(-1, u)
+        s2i = np.asarray(out.sigma2[i]).reshape(-1, u)
+        for tt in range(Ys.shape[1]):
+            g, m = O.gram_mrc(H[i].astype(complex), Ys[i, tt].astype(complex))
+            z, s2, _ = O.linear_equalize(kind, g, m, n0)
+            assert normwise_rel(zi[tt], z) < XHAT_TOL, (i, tt)
+            assert entry_rel(s2i[0], s2) < SIGMA2_TOL, (i, tt)

@@ -45,6 +45,24 @@ def test_lama_units(golden, name, bits):
     assert rel(zd, g[f"lama_{name}_damped_z"]) < TOL
 
 
+def test_lama_receive_domain_equals_gram_domain():
+    """Acceptance criterion 3 (test_acceptance.py:99-113) in float64: the
+    receive-domain recursion (oracle.lama_receive_domain) and the pinned
+    Gram-domain oracle give the same iterates on 20 instances."""
+    rng = np.random.default_rng(99)
+    syms, _ = O.square_qam(2)
+    b, u, n0 = 64, 16, 0.05
+    for _ in range(20):
+        h = (rng.standard_normal((b, u)) + 1j * rng.standard_normal((b, u))) / np.sqrt(2 * b)
+        s0 = syms[rng.integers(0, syms.size, u)]
+        y = h @ s0 + (rng.standard_normal(b) + 1j * rng.standard_normal(b)) * np.sqrt(n0 / 2)
+        gram, ym = O.gram_mrc(h, y)
+        _, _, tr = O.lama_equalize(gram, ym, syms, 1.0, n0, u / b, t_max=5, want_trace=True)
+        ref = O.lama_receive_domain(y, h, syms, n0, u / b, 5)
+        for st, (z, phi) in zip(tr, ref):
+            assert np.max(np.abs(st[1] - z)) < TOL and abs(st[4] - phi) < TOL
+
+
 def test_posterior_and_hard_units(golden):
     g = golden("units")
     for name, bits in (("qpsk", 2), ("qam16", 4), ("qam64", 6)):
