@@ -152,7 +152,7 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
 int launch_t2_stats_solve(EqParams& p, cudaStream_t st) {
   if (p.u > 16 || p.T > 16 || (p.kind != EQ_ZF && p.kind != EQ_LMMSE) || p.lama_scale != 1.f) return 1;
   if (opt(DBP_OPT_KERNEL) == DBP_KERNEL_SIMT) return 1;
-  const int work = align_up((16 + p.TP) * 18 * 8 + 32 * 8 + 16, 128);
+  const int work = align_up((16 + p.TP) * 18 * 8 + 32 * 8 + 16, 128) + 16;  // +16: see make_tc2_layout
   const int smem = 2 * T2S_WARPS * work;
   if (cudaFuncSetAttribute(t2_stats_solve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");

@@ -140,7 +140,8 @@ __host__ __device__ inline Tc2Layout make_tc2_layout(const Tc2Geom& g, int TP, i
     L.w.phi = L.w.coef = L.w.s2 = L.w.gn = L.w.dg = L.w.den = L.w.harm = L.w.wbuf = L.w.Z;
     L.w.total = align_up(q + 16, 128);
   }
-  L.work_stride = L.w.total;
+  // +16 bytes: the two half-warps' pivot-column buffers start 4 banks apart
+  L.work_stride = L.w.total + 16;
   o += T2_NWORK * L.work_stride;
   L.fdacc = o;
   L.fdacc_stride = fd ? t2_fdacc_bytes(g.T, C) : 0;
@@ -914,7 +915,8 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
           const float mine = __uint_as_float(gr[2 * v]);
           const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(gr[2 * v + 1]), 1);
           const float val = s_im ? (po - mine) : (mine + po);
-          if (uh < u && v < u) Gf[(uh * LD + v) * 2 + s_im] = val;
+          // stored as G[v][uh] = conj(G[uh][v]) (G is Hermitian): lanes hit 32 banks
+          if (uh < u && v < u) Gf[(v * LD + uh) * 2 + s_im] = s_im ? -val : val;
         }
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
