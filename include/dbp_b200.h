@@ -89,7 +89,7 @@ int dbp_last_kernel(void);
  * library reads the environment. */
 #define DBP_OPT_KERNEL 0      /* force a DBP_KERNEL_* (it must cover the geometry) */
 #define DBP_OPT_TC_SMAX_KB 1  /* tf32 kernel: max stage size (KB) */
-#define DBP_OPT_TC_NS 2       /* tf32 kernel: stage ring depth */
+#define DBP_OPT_TC_NS 2       /* tensor-core kernels: stage ring depth (cap) */
 #define DBP_OPT_TC_PAIR 3     /* tf32 kernel: units per operand tile (1, 2) */
 #define DBP_OPT_TC_NSOLV 4    /* tf32 kernel: solver warps */
 #define DBP_OPT_SIMT_NS 5     /* SIMT kernel: stage ring depth */

@@ -249,6 +249,177 @@ __device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, in
   linear_solve_warp_n<UP, 1>(&w, &a, &rho, lane);
 }
 
+// ---- blocked Gauss-Jordan inverse, U = 64, 256 threads --------------------
+// The same in-place sweep as the rank-1 version below (no pivoting, HPD),
+// eight pivots per step, so one CTA barrier per eight pivots and a
+// register-tiled rank-8 update.  Thread (ti, tj) = (tid / 16, tid % 16) owns
+// the 4 x 4 tile rows 4 ti .. 4 ti + 3, cols 4 tj .. 4 tj + 3; warp w owns rows
+// 8 w .. 8 w + 7.  For pivot block K = [8 b, 8 b + 8) with P = M[K,K],
+// Pinv = P^-1, C = M[:,K], R = M[K,:], one step is
+//     M <- M - Ct Rt,   Rt = R except Rt[:,K] = P + I,
+//                       Ct = C Pinv except Ct[K,:] = I - Pinv,
+// which gives Pinv on M[K,K], Pinv R on the pivot rows, -C Pinv on the pivot
+// columns and M - C Pinv R elsewhere (= eight rank-1 Gauss-Jordan steps).
+// Rt crosses warps (shared memory, double-buffered by block parity); every
+// warp inverts P itself (8 sequential pivots on its lanes, shuffles only) and
+// forms Ct for its own eight rows, whose C entries it already holds.  The
+// sequential pivots of P are those of the rank-1 sweep, so the singularity
+// test (pivot below 8 u eps of its original diagonal) is unchanged.  The
+// scratch (Rt, per-warp C / Pinv / Ct) lives in the G area, which is free
+// while the matrix sits in registers; A = M^-1 is written back to G at the
+// end.
+__device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, int tid) {
+  const int LD = w.LD;
+  const int ti = tid >> 4, tj = tid & 15, warp = tid >> 5, lane = tid & 31;
+  float2 m[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * ti + r, j = 4 * tj + c;
+      float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
+      if (i < u && j < u) {
+        v = w.G[i * LD + j];
+        if (i == j) {
+          v.x += rho;
+          v.y = 0.f;
+          w.dg[i] = v.x;
+        }
+      }
+      m[r][c] = v;
+    }
+  __syncthreads();  // G is scratch from here on
+  float2* rt = w.G;                            // [2][8][64]  Rt of the step (block parity)
+  float2* wsc = w.G + 2 * 8 * 64 + warp * 192;  // per warp: C [8][8], Pinv [8][8], Ct [8][8]
+  float2* cb = wsc;
+  float2* pb = wsc + 64;
+  float2* ctb = wsc + 128;
+  const float tolf = 8.f * (float)u * FLT_EPSILON;
+  bool bad = false;
+  const int nblk = (u + 7) >> 3;
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b) {
+    float2* rb = rt + (b & 1) * 512;
+    // publish Rt (the pivot rows, +I on the pivot block's diagonal) and this
+    // warp's C entries (its rows of the pivot columns)
+    if (warp == b) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int lr = 4 * (ti & 1) + r;
+        float2 v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          v[c] = m[r][c];
+          if (4 * tj + c == 8 * b + lr) v[c].x += 1.f;
+        }
+        *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+        *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj + 2) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+      }
+    }
+    if ((tj >> 1) == b) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int lr = 4 * (ti & 1) + r, c0 = 4 * (tj & 1);
+        *reinterpret_cast<float4*>(cb + lr * 8 + c0) = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
+        *reinterpret_cast<float4*>(cb + lr * 8 + c0 + 2) = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
+      }
+    }
+    __syncthreads();
+    // Pinv: lane l holds P[pr][pc], P[pr + 1][pc] (pr = 2 (l / 8), pc = l % 8)
+    {
+      const int pc = lane & 7, pr = 2 * (lane >> 3);
+      float2 q0 = rb[pr * 64 + 8 * b + pc], q1 = rb[(pr + 1) * 64 + 8 * b + pc];
+      if (pr == pc) q0.x -= 1.f;
+      if (pr + 1 == pc) q1.x -= 1.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int src_col = (pr >> 1) * 8 + k;   // lane holding (pr, k), (pr + 1, k)
+        const int src_row = (k >> 1) * 8 + pc;   // lane holding (k, pc)
+        const int src_piv = (k >> 1) * 8 + k;    // lane holding (k, k)
+        const float c0x = __shfl_sync(0xffffffffu, q0.x, src_col), c0y = __shfl_sync(0xffffffffu, q0.y, src_col);
+        const float c1x = __shfl_sync(0xffffffffu, q1.x, src_col), c1y = __shfl_sync(0xffffffffu, q1.y, src_col);
+        const float rkx = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_row);
+        const float rky = __shfl_sync(0xffffffffu, (k & 1) ? q1.y : q0.y, src_row);
+        float p = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_piv);
+        const int kg = 8 * b + k;
+        if (kg < u && !(p > tolf * w.dg[kg])) {
+          bad = true;
+          p = 1.f;
+        }
+        const float rp = __frcp_rn(p);
+        const float2 rj = (pc == k) ? make_float2(1.f + rp, 0.f) : make_float2(rkx * rp, rky * rp);
+        const float2 ci0 = (pr == k) ? make_float2(p - 1.f, 0.f) : make_float2(c0x, c0y);
+        const float2 ci1 = (pr + 1 == k) ? make_float2(p - 1.f, 0.f) : make_float2(c1x, c1y);
+        c_fms(q0, ci0, rj);
+        c_fms(q1, ci1, rj);
+      }
+      pb[pr * 8 + pc] = q0;
+      pb[(pr + 1) * 8 + pc] = q1;
+    }
+    __syncwarp();
+    // Ct for the warp's rows: lane -> row lr = lane / 4, columns 2 (lane % 4) + {0, 1}
+    {
+      const int lr = lane >> 2, c0 = 2 * (lane & 3);
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+      if (warp == b) {
+        const float4 pv = *reinterpret_cast<const float4*>(pb + lr * 8 + c0);
+        a0 = make_float2((lr == c0 ? 1.f : 0.f) - pv.x, -pv.y);
+        a1 = make_float2((lr == c0 + 1 ? 1.f : 0.f) - pv.z, -pv.w);
+      } else {
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const float2 cv = cb[lr * 8 + l];
+          const float4 pv = *reinterpret_cast<const float4*>(pb + l * 8 + c0);
+          c_fma(a0, cv, make_float2(pv.x, pv.y));
+          c_fma(a1, cv, make_float2(pv.z, pv.w));
+        }
+      }
+      *reinterpret_cast<float4*>(ctb + lr * 8 + c0) = make_float4(a0.x, a0.y, a1.x, a1.y);
+    }
+    __syncwarp();
+    // rank-8 update of the tile
+#pragma unroll
+    for (int l = 0; l < 8; l += 2) {
+      float2 cr[4][2], rr[2][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float4 v = *reinterpret_cast<const float4*>(ctb + (4 * (ti & 1) + r) * 8 + l);
+        cr[r][0] = make_float2(v.x, v.y);
+        cr[r][1] = make_float2(v.z, v.w);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float4 v0 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 4 * tj);
+        const float4 v1 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 4 * tj + 2);
+        rr[e][0] = make_float2(v0.x, v0.y);
+        rr[e][1] = make_float2(v0.z, v0.w);
+        rr[e][2] = make_float2(v1.x, v1.y);
+        rr[e][3] = make_float2(v1.z, v1.w);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          c_fms(m[r][c], cr[r][0], rr[0][c]);
+          c_fms(m[r][c], cr[r][1], rr[1][c]);
+        }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(w.flags, ST_SINGULAR);
+  __syncthreads();  // scratch reads done: write A = M^-1 back to G
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = 4 * ti + r;
+    if (i < u) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = 4 * tj + c;
+        if (j < u) w.G[i * LD + j] = m[r][c];
+      }
+    }
+  }
+}
+
 // ---- linear equalizers on (G, Z) -> X (per symbol), s2, gn --------------
 // equalize.py:130-176 (+ unbiased_output :179-195 when a.unbias).
 //  MRC  : d = Re G_ii; z = y/d; s2 = N0/d + Es sum_{j!=i}|G_ij|^2/d^2
@@ -293,92 +464,96 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     linear_solve_warp<UP>(w, a, rho, tid);
     return;
   }
-  // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows.  The
-  // sweep is the branch-free rank-1 update of linear_solve_warp_n
-  //   m_ij -= c_i r_j,  c_i = m_ik (i != k), c_k = p - 1,  r_j = m_kj / p (j != k), r_k = 1 + 1/p,
-  // with rotating register order: after every RS steps the row registers
-  // rotate by one, so the pivot row is always register 0; the pivot column
-  // is published by register slot ([i0][slot], slot = original register).
-  constexpr int RS = (NT >= UP) ? NT / UP : 1;
-  constexpr int EPT = (UP * UP + NT - 1) / NT;
-  static_assert((EPT & (EPT - 1)) == 0, "rows per thread must be a power of two");
-  const int j = tid % UP;
-  const int i0 = tid / UP;
-  const bool live = (i0 < UP);  // threads beyond UP*UP elements (NT > UP*UP) idle
-  float2 m[EPT];
-  float2* rowb = w.W;           // [2][UP] pivot rows (double-buffered)
-  float2* colb = w.W + 2 * UP;  // [2][UP] pivot columns, [i0][slot]
-  const float tolf = 8.f * (float)u * FLT_EPSILON;
-#pragma unroll
-  for (int r = 0; r < EPT; ++r) {
-    const int i = i0 + r * RS;
-    float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
-    if (i < u && j < u) {
-      v = w.G[i * LD + j];
-      if (i == j) {
-        v.x += rho;
-        v.y = 0.f;
-        w.dg[i] = v.x;
+  if constexpr (UP == 64 && NT == 256) {
+    gj64_blocked(w, u, rho, tid);  // eight pivots per barrier
+  } else {
+    // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows.  The
+    // sweep is the branch-free rank-1 update of linear_solve_warp_n
+    //   m_ij -= c_i r_j,  c_i = m_ik (i != k), c_k = p - 1,  r_j = m_kj / p (j != k), r_k = 1 + 1/p,
+    // with rotating register order: after every RS steps the row registers
+    // rotate by one, so the pivot row is always register 0; the pivot column
+    // is published by register slot ([i0][slot], slot = original register).
+    constexpr int RS = (NT >= UP) ? NT / UP : 1;
+    constexpr int EPT = (UP * UP + NT - 1) / NT;
+    static_assert((EPT & (EPT - 1)) == 0, "rows per thread must be a power of two");
+    const int j = tid % UP;
+    const int i0 = tid / UP;
+    const bool live = (i0 < UP);  // threads beyond UP*UP elements (NT > UP*UP) idle
+    float2 m[EPT];
+    float2* rowb = w.W;           // [2][UP] pivot rows (double-buffered)
+    float2* colb = w.W + 2 * UP;  // [2][UP] pivot columns, [i0][slot]
+    const float tolf = 8.f * (float)u * FLT_EPSILON;
+  #pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+      const int i = i0 + r * RS;
+      float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
+      if (i < u && j < u) {
+        v = w.G[i * LD + j];
+        if (i == j) {
+          v.x += rho;
+          v.y = 0.f;
+          w.dg[i] = v.x;
+        }
       }
+      m[r] = v;
     }
-    m[r] = v;
-  }
-  for (int k0 = 0; k0 < UP; k0 += RS) {
-    for (int kk = 0; kk < RS && k0 + kk < UP; ++kk) {
-      const int k = k0 + kk;
-      float2* rk = rowb + (k & 1) * UP;
-      float2* ck = colb + (k & 1) * UP;
-      if (live) {
-        if (i0 == kk) rk[j] = m[0];
-        if (j == k) {
-          // slot = register index: readers with the same i0 share the writer's
-          // rotation state, so register r of every such thread holds the same row
+    for (int k0 = 0; k0 < UP; k0 += RS) {
+      for (int kk = 0; kk < RS && k0 + kk < UP; ++kk) {
+        const int k = k0 + kk;
+        float2* rk = rowb + (k & 1) * UP;
+        float2* ck = colb + (k & 1) * UP;
+        if (live) {
+          if (i0 == kk) rk[j] = m[0];
+          if (j == k) {
+            // slot = register index: readers with the same i0 share the writer's
+            // rotation state, so register r of every such thread holds the same row
+            if constexpr (EPT >= 2) {
+  #pragma unroll
+              for (int r = 0; r < EPT; r += 2)
+                *reinterpret_cast<float4*>(ck + i0 * EPT + r) = make_float4(m[r].x, m[r].y, m[r + 1].x, m[r + 1].y);
+            } else {
+              ck[i0] = m[0];
+            }
+          }
+        }
+        tm.sync();
+        float p = rk[k].x;
+        if (k < u && !(p > tolf * w.dg[k])) {
+          if (tid == 0) set_status(w.flags, ST_SINGULAR);
+          p = 1.f;
+        }
+        if (k >= u) p = 1.f;  // padded step: identity pivot
+        const float rp = __frcp_rn(p);  // = 1.f / p (correctly rounded), no division slow path
+        if (live) {
+          const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rk[j], rp);
           if constexpr (EPT >= 2) {
-#pragma unroll
-            for (int r = 0; r < EPT; r += 2)
-              *reinterpret_cast<float4*>(ck + i0 * EPT + r) = make_float4(m[r].x, m[r].y, m[r + 1].x, m[r + 1].y);
+  #pragma unroll
+            for (int r = 0; r < EPT; r += 2) {
+              const float4 c2 = *reinterpret_cast<const float4*>(ck + i0 * EPT + r);
+              float2 ci = make_float2(c2.x, c2.y);
+              if (r == 0 && i0 == kk) ci = make_float2(p - 1.f, 0.f);
+              c_fms(m[r], ci, rj);
+              c_fms(m[r + 1], make_float2(c2.z, c2.w), rj);
+            }
           } else {
-            ck[i0] = m[0];
+            const float2 ci = (i0 == kk) ? make_float2(p - 1.f, 0.f) : ck[i0];
+            c_fms(m[0], ci, rj);
           }
         }
       }
-      tm.sync();
-      float p = rk[k].x;
-      if (k < u && !(p > tolf * w.dg[k])) {
-        if (tid == 0) set_status(w.flags, ST_SINGULAR);
-        p = 1.f;
-      }
-      if (k >= u) p = 1.f;  // padded step: identity pivot
-      const float rp = __frcp_rn(p);  // = 1.f / p (correctly rounded), no division slow path
       if (live) {
-        const float2 rj = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(rk[j], rp);
-        if constexpr (EPT >= 2) {
-#pragma unroll
-          for (int r = 0; r < EPT; r += 2) {
-            const float4 c2 = *reinterpret_cast<const float4*>(ck + i0 * EPT + r);
-            float2 ci = make_float2(c2.x, c2.y);
-            if (r == 0 && i0 == kk) ci = make_float2(p - 1.f, 0.f);
-            c_fms(m[r], ci, rj);
-            c_fms(m[r + 1], make_float2(c2.z, c2.w), rj);
-          }
-        } else {
-          const float2 ci = (i0 == kk) ? make_float2(p - 1.f, 0.f) : ck[i0];
-          c_fms(m[0], ci, rj);
-        }
+        const float2 first = m[0];
+  #pragma unroll
+        for (int r = 0; r + 1 < EPT; ++r) m[r] = m[r + 1];
+        m[EPT - 1] = first;
       }
     }
     if (live) {
-      const float2 first = m[0];
-#pragma unroll
-      for (int r = 0; r + 1 < EPT; ++r) m[r] = m[r + 1];
-      m[EPT - 1] = first;
-    }
-  }
-  if (live) {
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) {
-      const int i = i0 + r * RS;
-      if (i < u && j < u) w.G[i * LD + j] = m[r];
+  #pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int i = i0 + r * RS;
+        if (i < u && j < u) w.G[i * LD + j] = m[r];
+      }
     }
   }
   tm.sync();

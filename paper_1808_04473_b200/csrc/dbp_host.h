@@ -20,6 +20,9 @@ void* stream_scratch(cudaStream_t st, size_t need);  // per-(device, stream) scr
 // launchers: 0 launched, < 0 error, 1 geometry not covered (caller falls back)
 int launch_tc2(EqParams& p, cudaStream_t st);
 int launch_t2_stats_solve(EqParams& p, cudaStream_t st);
+// U = 64 statistics on the split-bf16 tensor cores; bf16 parts: 3 for the
+// statistics API (~3xTF32 accuracy), 2 inside PD equalization (x-hat ~2e-5)
+int launch_tcw(EqParams& p, cudaStream_t st, int nsplit_default = 3);
 int launch_tc_up(int up, EqParams& p, cudaStream_t st);
 int launch_stream_up(int up, EqParams& p, cudaStream_t st);
 int launch_stats_up(int up, EqParams& p, cudaStream_t st);

@@ -553,6 +553,11 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
                        (p.arch == ARCH_STATS || (p.arch == ARCH_PD && p.kind != EQ_LAMA));
   if (wide_ok) {
     if (p.arch == ARCH_STATS) {
+      if (pol != DBP_KERNEL_TC_TF32) {  // split-bf16 wide statistics kernel first
+        const int rc = launch_tcw(p, st);
+        if (rc == 0) g_last_kernel = DBP_KERNEL_TC_BF16;
+        if (rc <= 0) return rc;
+      }
       const int rc = launch_tc_up(64, p, st);
       if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
       if (rc <= 0) return rc;
@@ -563,10 +568,15 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
       const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
       q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
       if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
-      const int rc = launch_tc_up(64, q, st);
+      int kid = DBP_KERNEL_TC_BF16;
+      int rc = pol != DBP_KERNEL_TC_TF32 ? launch_tcw(q, st, 2) : 1;
+      if (rc == 1) {
+        kid = DBP_KERNEL_TC_TF32;
+        rc = launch_tc_up(64, q, st);
+      }
       if (rc < 0) return rc;
       if (rc == 0) {
-        g_last_kernel = DBP_KERNEL_TC_TF32;
+        g_last_kernel = kid;
         EqParams r = p;
         r.stats_in = q.stats_out;
         r.C = 1;

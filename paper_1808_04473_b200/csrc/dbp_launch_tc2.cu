@@ -14,6 +14,7 @@
 
 #include "../../include/dbp_b200.h"
 #include "dbp_host.h"
+#include "dbp_tcw.cuh"
 
 namespace dbp {
 
@@ -133,7 +134,8 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   g.NS = 2;
-  for (int ns = 8; ns > 2; --ns) {
+  const int ns_cap = opt(DBP_OPT_TC_NS) ? std::max(2, opt(DBP_OPT_TC_NS)) : 8;  // test / study override
+  for (int ns = ns_cap; ns > 2; --ns) {
     Tc2Geom t = g;
     t.NS = ns;
     if (make_tc2_layout(t, p.TP, p.C, fdm).total <= smem_max) {
@@ -161,6 +163,79 @@ int launch_t2_stats_solve(EqParams& p, cudaStream_t st) {
                                                               (int64_t)sm_count() * 8));
   t2_stats_solve_kernel<16><<<(unsigned)grid, 32 * T2S_WARPS, smem, st>>>(p, work);
   return cuda_check("t2_stats_solve_kernel");
+}
+
+// ---- wide statistics kernel (dbp_tcw.cuh): 32 < u <= 64, per-unit {G, y_mrc}
+// (summed over the clusters, or per uniform cluster); K a multiple of 32.
+// Returns 1 when the geometry is not covered (caller falls back).
+int launch_tcw(EqParams& p, cudaStream_t st, int nsplit_default) {
+  if (p.arch != ARCH_STATS || p.u <= 32 || p.u > 64 || p.us > 64 || p.T > 16) return 1;
+  const int upi = p.sum_clusters ? 1 : p.C;
+  if (p.B % upi) return 1;
+  const int K = p.B / upi;
+  if (K % 32) return 1;
+  for (int c = 0; c < upi && upi > 1; ++c) {  // uniform contiguous clusters only
+    int rows = 0;
+    for (int j = 0; j < p.nchunks; ++j)
+      if (p.chunks[j].cluster == c) {
+        if (p.chunks[j].row0 != c * K + rows) return 1;
+        rows += p.chunks[j].nrows;
+      }
+    if (rows != K) return 1;
+  }
+  if ((reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y)) & 15) return 1;
+  if ((p.us & 1) || (p.B & 1) || p.n_items > 0x7ffffff0) return 1;
+  auto enc = tensor_map_encoder();
+  if (!enc) return 1;
+  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : nsplit_default;
+  if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
+  TcwGeom g;
+  memset(&g, 0, sizeof(g));
+  g.K = K;
+  g.nchunk = K / 32;
+  g.upi = upi;
+  g.T = p.T;
+  g.n_units = p.n_items * upi;
+  g.stage_bytes = align_up(std::max(TW_HBYTES + p.T * TW_YROW * 4, nsplit * TW_SPLIT), 1024);
+  CUtensorMap hm, ym;
+  {
+    // H as [item][antenna][2 us floats]; box = 32 antennas x 128 floats (zero fill past 2 us)
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * p.us, (cuuint64_t)p.B, (cuuint64_t)p.n_items};
+    const cuuint64_t strides[2] = {(cuuint64_t)2 * p.us * 4, (cuuint64_t)p.B * 2 * p.us * 4};
+    const cuuint32_t box[3] = {128, 32, 1}, es[3] = {1, 1, 1};
+    if (enc(&hm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(p.H), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 1;
+  }
+  {
+    // Y as [item][T][2B floats]; box = T rows x 64 floats (32 antennas)
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * p.B, (cuuint64_t)p.T, (cuuint64_t)p.n_items};
+    const cuuint64_t strides[2] = {(cuuint64_t)2 * p.B * 4, (cuuint64_t)2 * p.T * p.B * 4};
+    const cuuint32_t box[3] = {TW_YROW, (cuuint32_t)p.T, 1}, es[3] = {1, 1, 1};
+    if (enc(&ym, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(p.Y), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 1;
+  }
+  int dev = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int ns_cap = opt(DBP_OPT_TC_NS) ? std::max(2, opt(DBP_OPT_TC_NS)) : 8;
+  g.NS = 0;
+  for (int ns = ns_cap; ns >= 2; --ns)
+    if (tcw_bars_bytes(ns) + ns * g.stage_bytes <= smem_max) {
+      g.NS = ns;
+      break;
+    }
+  if (!g.NS) return 1;
+  const int smem = tcw_bars_bytes(g.NS) + g.NS * g.stage_bytes;
+  auto kern = nsplit == 2 ? tcw_stats_kernel<2> : tcw_stats_kernel<3>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return fail(DBP_E_CUDA, "shared memory request too large");
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(g.n_units, (int64_t)sm_count()));
+  kern<<<(unsigned)grid, TW_THREADS, smem, st>>>(p, hm, ym, g);
+  return cuda_check("tcw_stats_kernel");
 }
 
 }  // namespace dbp

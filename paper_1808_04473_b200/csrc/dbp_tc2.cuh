@@ -51,8 +51,12 @@
 
 // timing-study ablations (study builds only: make study): 1 solvers skip the
 // epilogue, 2 no MMAs, 4 converters skip the conversion
-#ifdef DBP_STUDY
+#if defined(DBP_STUDY) && !defined(T2X_NOABL)
 #define T2_ABLATE(bit) (p.ablate & (bit))
+#else
+#define T2_ABLATE(bit) false
+#endif
+#if defined(DBP_STUDY) && !defined(T2X_NOCLK)
 // per-warp wait-cycle counters (DBP_TC_DEBUG): [warp][total, wait1, wait2, -]
 #define T2_WAIT(bar, par, slot)           \
   do {                                    \
@@ -60,9 +64,24 @@
     mbar_wait(bar, par);                  \
     dbgc[slot] += clock64() - t0_;        \
   } while (0)
+#elif defined(T2X_CLKMASK)
+#define T2_WAIT(bar, par, slot) T2_WAITR(bar, par, slot, 15)
 #else
-#define T2_ABLATE(bit) false
 #define T2_WAIT(bar, par, slot) mbar_wait(bar, par)
+#endif
+#if defined(T2X_CLKMASK)
+#define T2_WAITR(bar, par, slot, role)                 \
+  do {                                                 \
+    if (T2X_CLKMASK & (role)) {                        \
+      const long long t0_ = clock64();                 \
+      mbar_wait(bar, par);                             \
+      dbgc[slot] += clock64() - t0_;                   \
+    } else {                                           \
+      mbar_wait(bar, par);                             \
+    }                                                  \
+  } while (0)
+#else
+#define T2_WAITR(bar, par, slot, role) T2_WAIT(bar, par, slot)
 #endif
 
 #include "dbp_tc.cuh"
@@ -296,6 +315,22 @@ struct T2FdAcc {
   int* st;      // status of the item (first failing cluster's code)
 };
 
+// Gauss-Jordan steps per unrolled frame of t2_solve_pair (register rotation
+// by T2_GJU after each frame)
+#ifndef T2_GJU
+#define T2_GJU 4
+#endif
+static_assert(16 % T2_GJU == 0, "frame must divide 16");
+__device__ __forceinline__ void t2_rotate(float2 (&m)[16]) {
+  float2 t[T2_GJU];
+#pragma unroll
+  for (int i = 0; i < T2_GJU; ++i) t[i] = m[i];
+#pragma unroll
+  for (int i = 0; i < 16 - T2_GJU; ++i) m[i] = m[i + T2_GJU];
+#pragma unroll
+  for (int i = 0; i < T2_GJU; ++i) m[16 - T2_GJU + i] = t[i];
+}
+
 // Two units per warp, one per half-warp: MRC / ZF / L-MMSE (equalize.py:130-
 // 195).  Lane (h = lane / 16, j = lane % 16) owns column j of unit h's matrix
 // M = G + rho I (all 16 rows in registers).  ZF / L-MMSE: in-place
@@ -345,26 +380,21 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   bool bad = false;
   if (!mrc) {
     const float tolf = 8.f * (float)u * FLT_EPSILON;
-    // Rotating register order: at step k the lane's row-k element is m[k % 4]
-    // of the current frame, and after every 4 steps the registers rotate by
-    // 4, so all indices stay static with a 4-step unrolled body; the pivot
-    // column is published and read in the same frame.  Padded steps (k >= u)
-    // are identity pivots and no-ops: whole groups of 4 of them are skipped
-    // and replaced by the bare register rotation that restores the frame.
+    // Rotating register order: at step k the lane's row-k element is
+    // m[k % T2_GJU] of the current frame, and after every T2_GJU steps the
+    // registers rotate by T2_GJU, so all indices stay static within an
+    // unrolled frame; the pivot column is published and read in the same
+    // frame.  Padded steps (k >= u) are identity pivots and no-ops: whole
+    // frames of them are skipped and replaced by the bare register rotation
+    // that restores the order.
 #pragma unroll 1
-    for (int k0 = 0; k0 < 16; k0 += 4) {
+    for (int k0 = 0; k0 < 16; k0 += T2_GJU) {
       if (k0 >= u) {
-        float2 t4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) t4[i] = m[i];
-#pragma unroll
-        for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
+        t2_rotate(m);
         continue;
       }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < T2_GJU; ++kk) {
         const int k = k0 + kk;
         float2* cb = colb + (kk & 1) * 16;
         if (j == k) {  // publish the pivot column (a failed pivot is replaced by 1)
@@ -394,13 +424,7 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
 #pragma unroll
         for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
       }
-      float2 t4[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) t4[i] = m[i];
-#pragma unroll
-      for (int i = 0; i < 12; ++i) m[i] = m[i + 4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) m[12 + i] = t4[i];
+      t2_rotate(m);
     }
   }
   // per-lane scalars: A_jj (ZF / L-MMSE) or d = G_jj and the off-diagonal
@@ -629,7 +653,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-#ifdef DBP_STUDY
+#if defined(DBP_STUDY) || defined(T2X_CLKMASK)
   long long dbgc[4] = {0, 0, 0, 0};
   const long long t_start = clock64();
 #endif
@@ -671,7 +695,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       int s = 0;
       uint32_t ph = 0;
       for (int sq = 0; sq < total; ++sq) {
-        if (sq >= NS) T2_WAIT(&stage_empty[s], ph ^ 1u, 1);
+        if (sq >= NS) T2_WAITR(&stage_empty[s], ph ^ 1u, 1, 1);
         int j, item0, c0;
         coords(sq, j, item0, c0);
         const uint32_t bar = smem_u32(&raw_full[s]);
@@ -702,12 +726,12 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
         int lb, cg;
         t2_group(gl, g.upi, nblocks, lb, cg);
         const int a = lb & 1;  // item blocks alternate accumulators
-        if (uses[a] >= 1) T2_WAIT(&acc_empty[a], (uint32_t)((uses[a] - 1) & 1), 2);
+        if (uses[a] >= 1) T2_WAITR(&acc_empty[a], (uint32_t)((uses[a] - 1) & 1), 2, 2);
         ++uses[a];
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(256 * a);
         for (int j = 0; j < nch; ++j) {
-          T2_WAIT(&conv_full[s], ph, 1);
+          T2_WAITR(&conv_full[s], ph, 1, 2);
           tc_fence_after();
           const uint32_t base = stg0 + (uint32_t)(s * g.stage_bytes);
 #pragma unroll
@@ -772,7 +796,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     uint32_t ph = 0;
     for (int gl = 0; gl < ngroups; ++gl) {
       for (int j = 0; j < nch; ++j) {
-        T2_WAIT(&raw_full[s], ph, 1);
+        T2_WAITR(&raw_full[s], ph, 1, 4);
         char* st = smem + L.stg + s * g.stage_bytes;
         if (T2_ABLATE(4)) {
           __syncwarp();
@@ -894,7 +918,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
         n[k] = (b_first + lb) * 4 + q;
         valid[k] = n[k] < g.n_items;
         if (valid[k] && MODE != T2_STATS) n0[k] = item_n0(p, n[k]);  // global load before the wait
-        T2_WAIT(&acc_full[sset], (uint32_t)(use & 1), 1);
+        T2_WAITR(&acc_full[sset], (uint32_t)(use & 1), 1, 8);
         ++use;
         tc_fence_after();
         uint32_t gr[32], yr[32];

@@ -141,6 +141,24 @@ class TestLinearEqualize:
         with pytest.raises(SingularGramError):
             dbp.linear_equalize("zf", stats, 0.1)
 
+    @pytest.mark.parametrize("u", [16, 40, 64])
+    def test_zf_rank_deficient_batch(self, u):
+        """B = u / 2 antennas: every item's Gram has rank u / 2 (ZF singular,
+        the solvers of u <= 16, 17..32 and the blocked 64-wide sweep), while
+        L-MMSE on the same statistics stays regular."""
+        rng = np.random.default_rng(u)
+        b = u // 2
+        h = (rng.standard_normal((5, b, u)) + 1j * rng.standard_normal((5, b, u))) / np.sqrt(2 * b)
+        y = (rng.standard_normal((5, b)) + 1j * rng.standard_normal((5, b))) * 0.1
+        stats = dbp.centralized_stats(h, y)
+        with pytest.raises(SingularGramError):
+            dbp.linear_equalize("zf", stats, 0.1)
+        out = dbp.linear_equalize("lmmse", stats, 0.1)
+        for i in range(5):
+            g, m = O.gram_mrc(h[i], y[i])
+            z, s2, _ = O.linear_equalize("lmmse", g, m, 0.1)
+            assert rel(out.z[i], z) < 1e-4 and rel(out.sigma2[i], s2) < 1e-4
+
     def test_mrc_zero_diagonal(self):
         stats = FusedStats(gram=np.zeros((2, 2), dtype=complex), y_mrc=np.zeros(2, dtype=complex))
         with pytest.raises(SingularGramError):
