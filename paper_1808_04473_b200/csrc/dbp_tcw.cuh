@@ -24,14 +24,17 @@
 // conjugate-transposed (G is Hermitian), so every warp store is 128
 // contiguous bytes.
 //
-// Roles: warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 converters,
-// warps 6-9 epilogue.  Persistent: one CTA per SM, contiguous unit ranges.
+// Roles: warp 0 TMA producer, warp 1 MMA issuer, TW_NCONV converter warps,
+// four epilogue warps.  Persistent: one CTA per SM, contiguous unit ranges.
 #pragma once
 #include "dbp_tc2.cuh"
 
 namespace dbp {
 
-constexpr int TW_NCONV = 4;
+#ifndef DBP_TW_NCONV
+#define DBP_TW_NCONV 8
+#endif
+constexpr int TW_NCONV = DBP_TW_NCONV;  // converter warps (4 or 8)
 constexpr int TW_FIRST_CONV = 2;
 constexpr int TW_FIRST_EPI = TW_FIRST_CONV + TW_NCONV;
 constexpr int TW_NEPI = 4;
@@ -51,12 +54,6 @@ struct TcwGeom {
 };
 
 __host__ __device__ inline int tcw_bars_bytes(int NS) { return align_up((3 * NS + 4) * 8 + 16, 1024); }
-
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
-               : "memory");
-}
 
 template <int NSPLIT>
 __global__ void __launch_bounds__(TW_THREADS, 1)
@@ -110,12 +107,6 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         const int c = (int)(un - (int64_t)item * g.upi);
         a0 = c * g.K + 32 * j;  // first antenna of the stage
       };
-      for (int sq = NS; sq < 2 * NS && sq < total; ++sq) {
-        int a0, item;
-        coords(sq, a0, item);
-        tma_prefetch_3d(&hmap, 0, a0, item);
-        tma_prefetch_3d(&ymap, 2 * a0, 0, item);
-      }
       int s = 0;
       uint32_t ph = 0;
       for (int sq = 0; sq < total; ++sq) {
@@ -127,12 +118,6 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
         const uint32_t dst = stg0 + (uint32_t)(s * g.stage_bytes);
         tma_load_3d(dst, &hmap, 0, a0, item, bar, policy);
         tma_load_3d(dst + TW_HBYTES, &ymap, 2 * a0, 0, item, bar, policy);
-        if (sq + 2 * NS < total) {
-          int b0, it2;
-          coords(sq + 2 * NS, b0, it2);
-          tma_prefetch_3d(&hmap, 0, b0, it2);
-          tma_prefetch_3d(&ymap, 2 * b0, 0, it2);
-        }
         if (++s == NS) {
           s = 0;
           ph ^= 1u;
@@ -166,7 +151,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
             for (int pr = 0; pr < NP; ++pr) {
               const uint64_t da = umma_desc_mn16(base + PA[pr] * TW_SPLIT + ks * 2048);
               const uint64_t db = umma_desc_mn16(base + PB[pr] * TW_SPLIT + ks * 2048);
-              umma_bf16(d, da, db, idesc, (j | ks | pr) ? 1u : 0u);
+              if (!T2_ABLATE(2)) umma_bf16(d, da, db, idesc, (j | ks | pr) ? 1u : 0u);
             }
           }
           umma_commit(&stage_empty[s]);
@@ -183,7 +168,12 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
     // -------------------------------------------------------- converters ----
     const int ct = tid - 32 * TW_FIRST_CONV;
     const int T = g.T;
-    // H task i: quad jq (features 4 jq .. 4 jq + 3) of antenna row k = ct / 32 + 4 i
+    constexpr int RSTEP = TW_CT / 32;   // antenna rows (H) / symbol pairs (Y) per task round
+    constexpr int HT = 32 / RSTEP;      // H tasks per thread
+    constexpr int YT = 8 / RSTEP;       // Y tasks per thread (T <= 16: 8 symbol pairs)
+    static_assert(HT >= 1 && YT >= 1, "converter task split");
+    // H task i: quad jq (features 4 jq .. 4 jq + 3) of antenna row k0 + RSTEP i;
+    // Y task i: symbol pair tp = k0 + RSTEP i (symbols 2 tp, 2 tp + 1) of antenna jq
     const int jq = ct & 31, k0 = ct >> 5;
     int s = 0;
     uint32_t ph = 0;
@@ -193,32 +183,40 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
       char* st = stages + s * g.stage_bytes;
       const float* sf = reinterpret_cast<const float*>(st);
       const float* yf = sf + TW_HBYTES / 4;
-      float4 hv[8];
+      float4 hv[HT];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) hv[i] = *reinterpret_cast<const float4*>(sf + (k0 + 4 * i) * 128 + 4 * jq);
-      // Y task i: symbol pair tp = k0 + 4 i (symbols 2 tp, 2 tp + 1) of antenna jq
-      float2 ya[2], yb[2];
+      for (int i = 0; i < HT; ++i) hv[i] = *reinterpret_cast<const float4*>(sf + (k0 + RSTEP * i) * 128 + 4 * jq);
+      float2 ya[YT], yb[YT];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int tp = k0 + 4 * i;
+      for (int i = 0; i < YT; ++i) {
+        const int tp = k0 + RSTEP * i;
         ya[i] = (2 * tp < T) ? *reinterpret_cast<const float2*>(yf + (2 * tp) * TW_YROW + 2 * jq) : make_float2(0.f, 0.f);
         yb[i] = (2 * tp + 1 < T) ? *reinterpret_cast<const float2*>(yf + (2 * tp + 1) * TW_YROW + 2 * jq)
                                  : make_float2(0.f, 0.f);
       }
       named_bar(1, TW_CT);  // the whole slot is in registers: overwrite it in place
+      if (T2_ABLATE(4)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv_full[s]);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+        continue;
+      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < HT; ++i) {
         uint32_t w0[NSPLIT], w1[NSPLIT];
         split2<NSPLIT>(hv[i].x, hv[i].y, w0);
         split2<NSPLIT>(hv[i].z, hv[i].w, w1);
-        const int off = t2_off(jq >> 4, k0 + 4 * i, 4 * (jq & 15));
+        const int off = t2_off(jq >> 4, k0 + RSTEP * i, 4 * (jq & 15));
 #pragma unroll
         for (int sp = 0; sp < NSPLIT; ++sp)
           *reinterpret_cast<uint2*>(st + sp * TW_SPLIT + off) = make_uint2(w0[sp], w1[sp]);
       }
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int tp = k0 + 4 * i;
+      for (int i = 0; i < YT; ++i) {
+        const int tp = k0 + RSTEP * i;
         uint32_t w0[NSPLIT], w1[NSPLIT];
         split2<NSPLIT>(ya[i].x, ya[i].y, w0);
         split2<NSPLIT>(yb[i].x, yb[i].y, w1);
@@ -262,6 +260,7 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[a]);
         }
+        if (T2_ABLATE(1)) continue;
 #pragma unroll
         for (int v = 0; v < 16; ++v) {
           const float mine = __uint_as_float(r[2 * v]);
