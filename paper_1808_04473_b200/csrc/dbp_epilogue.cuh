@@ -260,14 +260,18 @@ __device__ void linear_solve_warp(const Work& w, const EpiArgs& a, float rho, in
 //                       Ct = C Pinv except Ct[K,:] = I - Pinv,
 // which gives Pinv on M[K,K], Pinv R on the pivot rows, -C Pinv on the pivot
 // columns and M - C Pinv R elsewhere (= eight rank-1 Gauss-Jordan steps).
-// Rt crosses warps (shared memory, double-buffered by block parity); every
-// warp inverts P itself (8 sequential pivots on its lanes, shuffles only) and
-// forms Ct for its own eight rows, whose C entries it already holds.  The
-// sequential pivots of P are those of the rank-1 sweep, so the singularity
-// test (pivot below 8 u eps of its original diagonal) is unchanged.  The
-// scratch (Rt, per-warp C / Pinv / Ct) lives in the G area, which is free
-// while the matrix sits in registers; A = M^-1 is written back to G at the
-// end.
+// Warp b owns the pivot rows of block b: right after its update for block
+// b - 1 it publishes Rt_b and, with `lookahead`, inverts P_b (eight
+// sequential pivots on its lanes, shuffles only) while the other warps reach
+// the barrier -- the better choice with two CTAs per SM (stats_kernel);
+// without it every warp inverts P_b itself after the barrier (one CTA per SM,
+// the streaming kernel: no warp idles).  Every warp then forms Ct for its own
+// eight rows, whose C entries it holds itself.  The sequential pivots of P are those of the rank-1 sweep,
+// so the singularity test (pivot below 8 u eps of its original diagonal) is
+// unchanged.  The scratch (Rt and Pinv, double-buffered by block parity, and
+// per-warp C / Ct) lives in the G area, free while the matrix sits in
+// registers; A = M^-1 is written back to G at the end.
+template <bool lookahead>
 __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, int tid) {
   const int LD = w.LD;
   const int ti = tid >> 4, tj = tid & 15, warp = tid >> 5, lane = tid & 31;
@@ -289,33 +293,80 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
       m[r][c] = v;
     }
   __syncthreads();  // G is scratch from here on
-  float2* rt = w.G;                            // [2][8][64]  Rt of the step (block parity)
-  float2* wsc = w.G + 2 * 8 * 64 + warp * 192;  // per warp: C [8][8], Pinv [8][8], Ct [8][8]
-  float2* cb = wsc;
-  float2* pb = wsc + 64;
-  float2* ctb = wsc + 128;
+  float2* rt = w.G;                                  // [2][8][64]  Rt of the step (block parity)
+  float2* pinvb = w.G + 2 * 512;                     // [2][8][8]   Pinv of the step (look-ahead)
+  float2* cb = w.G + 2 * 512 + 2 * 64 + warp * 192;  // per warp: C [8][8], Ct [8][8], own Pinv [8][8]
+  float2* ctb = cb + 64;
+  float2* pown = cb + 128;
   const float tolf = 8.f * (float)u * FLT_EPSILON;
-  bool bad = false;
   const int nblk = (u + 7) >> 3;
+  bool bad = false;
+  // warp b: publish Rt_b from its rows
+  auto publish = [&](int b) {
+    float2* rb = rt + (b & 1) * 512;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int lr = 4 * (ti & 1) + r;
+      float2 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        v[c] = m[r][c];
+        if (4 * tj + c == 8 * b + lr) v[c].x += 1.f;
+      }
+      *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+      *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj + 2) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+    }
+  };
+  // Pinv_b = (Rt_b[:, K] - I)^-1 into pb (one warp)
+  auto invert = [&](int b, float2* pb) {
+    const float2* rb = rt + (b & 1) * 512;
+    // lane l holds P[pr][pc], P[pr + 1][pc] (pr = 2 (l / 8), pc = l % 8)
+    const int pc = lane & 7, pr = 2 * (lane >> 3);
+    float2 q0 = rb[pr * 64 + 8 * b + pc], q1 = rb[(pr + 1) * 64 + 8 * b + pc];
+    if (pr == pc) q0.x -= 1.f;
+    if (pr + 1 == pc) q1.x -= 1.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int src_col = (pr >> 1) * 8 + k;  // lane holding (pr, k), (pr + 1, k)
+      const int src_row = (k >> 1) * 8 + pc;  // lane holding (k, pc)
+      const int src_piv = (k >> 1) * 8 + k;   // lane holding (k, k)
+      const float c0x = __shfl_sync(0xffffffffu, q0.x, src_col), c0y = __shfl_sync(0xffffffffu, q0.y, src_col);
+      const float c1x = __shfl_sync(0xffffffffu, q1.x, src_col), c1y = __shfl_sync(0xffffffffu, q1.y, src_col);
+      const float rkx = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_row);
+      const float rky = __shfl_sync(0xffffffffu, (k & 1) ? q1.y : q0.y, src_row);
+      float p = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_piv);
+      const int kg = 8 * b + k;
+      if (kg < u && !(p > tolf * w.dg[kg])) {
+        bad = true;
+        p = 1.f;
+      }
+      const float rp = __frcp_rn(p);
+      const float2 rj = (pc == k) ? make_float2(1.f + rp, 0.f) : make_float2(rkx * rp, rky * rp);
+      const float2 ci0 = (pr == k) ? make_float2(p - 1.f, 0.f) : make_float2(c0x, c0y);
+      const float2 ci1 = (pr + 1 == k) ? make_float2(p - 1.f, 0.f) : make_float2(c1x, c1y);
+      c_fms(q0, ci0, rj);
+      c_fms(q1, ci1, rj);
+    }
+    pb[pr * 8 + pc] = q0;
+    pb[(pr + 1) * 8 + pc] = q1;
+  };
+  if (warp == 0) {
+    publish(0);
+    if constexpr (lookahead) {
+      __syncwarp();
+      invert(0, pinvb);
+    }
+  }
+  __syncthreads();
 #pragma unroll 1
   for (int b = 0; b < nblk; ++b) {
-    float2* rb = rt + (b & 1) * 512;
-    // publish Rt (the pivot rows, +I on the pivot block's diagonal) and this
-    // warp's C entries (its rows of the pivot columns)
-    if (warp == b) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int lr = 4 * (ti & 1) + r;
-        float2 v[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          v[c] = m[r][c];
-          if (4 * tj + c == 8 * b + lr) v[c].x += 1.f;
-        }
-        *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
-        *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj + 2) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
-      }
+    const float2* rb = rt + (b & 1) * 512;
+    const float2* pb = pinvb + (b & 1) * 64;
+    if constexpr (!lookahead) {  // every warp inverts P_b itself (no warp idles at the barrier)
+      invert(b, pown);
+      pb = pown;
     }
+    // this warp's rows of the pivot columns
     if ((tj >> 1) == b) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -323,38 +374,6 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
         *reinterpret_cast<float4*>(cb + lr * 8 + c0) = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
         *reinterpret_cast<float4*>(cb + lr * 8 + c0 + 2) = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
       }
-    }
-    __syncthreads();
-    // Pinv: lane l holds P[pr][pc], P[pr + 1][pc] (pr = 2 (l / 8), pc = l % 8)
-    {
-      const int pc = lane & 7, pr = 2 * (lane >> 3);
-      float2 q0 = rb[pr * 64 + 8 * b + pc], q1 = rb[(pr + 1) * 64 + 8 * b + pc];
-      if (pr == pc) q0.x -= 1.f;
-      if (pr + 1 == pc) q1.x -= 1.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int src_col = (pr >> 1) * 8 + k;   // lane holding (pr, k), (pr + 1, k)
-        const int src_row = (k >> 1) * 8 + pc;   // lane holding (k, pc)
-        const int src_piv = (k >> 1) * 8 + k;    // lane holding (k, k)
-        const float c0x = __shfl_sync(0xffffffffu, q0.x, src_col), c0y = __shfl_sync(0xffffffffu, q0.y, src_col);
-        const float c1x = __shfl_sync(0xffffffffu, q1.x, src_col), c1y = __shfl_sync(0xffffffffu, q1.y, src_col);
-        const float rkx = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_row);
-        const float rky = __shfl_sync(0xffffffffu, (k & 1) ? q1.y : q0.y, src_row);
-        float p = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_piv);
-        const int kg = 8 * b + k;
-        if (kg < u && !(p > tolf * w.dg[kg])) {
-          bad = true;
-          p = 1.f;
-        }
-        const float rp = __frcp_rn(p);
-        const float2 rj = (pc == k) ? make_float2(1.f + rp, 0.f) : make_float2(rkx * rp, rky * rp);
-        const float2 ci0 = (pr == k) ? make_float2(p - 1.f, 0.f) : make_float2(c0x, c0y);
-        const float2 ci1 = (pr + 1 == k) ? make_float2(p - 1.f, 0.f) : make_float2(c1x, c1y);
-        c_fms(q0, ci0, rj);
-        c_fms(q1, ci1, rj);
-      }
-      pb[pr * 8 + pc] = q0;
-      pb[(pr + 1) * 8 + pc] = q1;
     }
     __syncwarp();
     // Ct for the warp's rows: lane -> row lr = lane / 4, columns 2 (lane % 4) + {0, 1}
@@ -404,9 +423,18 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
           c_fms(m[r][c], cr[r][1], rr[1][c]);
         }
     }
+    __syncwarp();  // the warp's Ct / C / Pinv reads are done before the next block rewrites them
+    if (warp == b + 1 && b + 1 < nblk) {
+      publish(b + 1);
+      if constexpr (lookahead) {
+        __syncwarp();
+        invert(b + 1, pinvb + ((b + 1) & 1) * 64);
+      }
+    }
+    __syncthreads();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(w.flags, ST_SINGULAR);
-  __syncthreads();  // scratch reads done: write A = M^-1 back to G
+  // (the last barrier of the loop: every scratch read is done)
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int i = 4 * ti + r;
@@ -435,7 +463,9 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
 // 8*u*eps of its original diagonal is SingularGramError: the fp32 counterpart
 // of zpotrf's "not positive definite" (a rank-deficient fp32 Gram leaves
 // rounding noise ~eps*G_jj instead of an exact zero).
-template <int UP, class TM>
+// LA: the blocked U = 64 solve inverts each pivot block on one warp (look-ahead;
+// for kernels with two CTAs per SM), else on every warp
+template <int UP, class TM, bool LA = false>
 __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
   constexpr int NT = TM::N;
   const int tid = tm.t;
@@ -465,7 +495,7 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     return;
   }
   if constexpr (UP == 64 && NT == 256) {
-    gj64_blocked(w, u, rho, tid);  // eight pivots per barrier
+    gj64_blocked<LA>(w, u, rho, tid);  // eight pivots per barrier
   } else {
     // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows.  The
     // sweep is the branch-free rank-1 update of linear_solve_warp_n
@@ -855,7 +885,7 @@ __device__ __forceinline__ void write_status(const Work& w, const EqParams& p, i
 // CLS: equalizer class known at compile time (0 stats only, 1 linear, 2 LAMA)
 // so a kernel instantiated for one class carries no code of the others; -1
 // decides at run time (SIMT kernels).
-template <int UP, class TM, int CLS = -1>
+template <int UP, class TM, int CLS = -1, bool LA = false>
 __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int cluster, bool item_end,
                               int& cl_first, const TM& tm, long long* dbg_solve = nullptr,
                               float n0_pre = -1.f) {
@@ -911,7 +941,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
       lama_unit<UP>(w, a, p.cp, tz, ts, tv, tp, tm, p.g_hermitian != 0);
     } else {
       const long long t0 = dbg_solve ? clock64() : 0;
-      linear_unit<UP>(w, a, tm);
+      linear_unit<UP, TM, LA>(w, a, tm);
       if (dbg_solve) *dbg_solve += clock64() - t0;
     }
     if (u == UP) {  // shifts instead of divisions
@@ -951,7 +981,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
   if (lama)
     lama_unit<UP>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, p.g_hermitian != 0);
   else
-    linear_unit<UP>(w, a, tm);
+    linear_unit<UP, TM, LA>(w, a, tm);
   // weights: MRC -> Gram diagonal (fusion.py:149-151), otherwise
   // 1/max(sigma2, 1e-15) (fusion.py:96-105); sigma2 <= 0 is a ConfigError
   const int wdim = lama ? T : u;

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqPar
       for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
     }
     __syncthreads();
-    unit_epilogue<UP>(w, p, n, 0, true, cl_first, tm);
+    unit_epilogue<UP, Team<NT, 0>, -1, true>(w, p, n, 0, true, cl_first, tm);  // two CTAs per SM: look-ahead solve
     __syncthreads();
   }
 }
