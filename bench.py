@@ -6,8 +6,8 @@ cfg2 = PD L-MMSE, B=128 antennas in C=4 clusters of 32, U=16 UEs, 16-QAM,
 W=1200 subcarriers x T=14 OFDM symbols, SNR 0..20 dB in 2 dB steps.  One
 step = one pass of the hot path over one batch: the 11 frames (one per SNR
 point) = 13,200 (subcarrier, frame) items x 14 symbols, in ONE fused kernel
-launch (Gram + matched filter + regularized Cholesky solve + unbiasing +
-hard demap).
+launch (Gram + matched filter + regularized solve (Gauss-Jordan inverse) +
+unbiasing + hard demap).
 
 metric: detected Gb/s = frames x W x T x U x log2(M) / device time.
 Prints ONE JSON line (rank 0).  --impl reference times the reference
@@ -282,6 +282,9 @@ def kernel_name(kernel_id, wl, two_pass):
     up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
     tag = f"{wl['arch'].upper()}-{wl['kind']}"
     if two_pass:
+        if kernel_id == 3:
+            return ("dbp::tcw_stats_kernel (split-bf16 tensor cores, one unit per M=128 x N=160 MMA) + "
+                    "dbp::stats_kernel<64> (blocked Gauss-Jordan solves)")
         return "dbp::tc_kernel<64, stats> (3xTF32 tensor cores, wide layout) + dbp::stats_kernel<64> (solves)"
     if kernel_id == 3:
         return f"dbp::tc2_kernel<{tag}> (split-bf16 tensor cores)"
@@ -405,7 +408,7 @@ def single_gpu(args, wl, name):
                 det.run(*copies[k % len(copies)], 0.0, n0_dev, W)
             torch.cuda.synchronize()
     kernel_id = _lib.lib().dbp_last_kernel()
-    two_pass = kernel_id == 2 and wl["U"] == 64 and wl["arch"] == "pd"  # statistics + solve launches
+    two_pass = kernel_id in (2, 3) and wl["U"] == 64 and wl["arch"] == "pd"  # statistics + solve launches
     launches = timed_launches * (2 if two_pass else 1)
     ms = elapsed_ms / args.steps
     bits = bits_per_step(wl)

@@ -261,17 +261,40 @@ __global__ void __launch_bounds__(TW_THREADS, 1)
           if (lane == 0) mbar_arrive(&acc_empty[a]);
         }
         if (T2_ABLATE(1)) continue;
+        // lane (ue, s_im) forms component s_im of G[ue][w] (or y_mrc[t][ue]):
+        // re = P[2ue][2w] + P[2ue+1][2w+1], im = P[2ue][2w+1] - P[2ue+1][2w];
+        // G goes out conjugate-transposed, G[w][ue] = re - i im: one FFMA each
+        const float sg = s_im ? -1.f : 1.f;
+        if (u == 64) {  // full tiles: fixed strides, no bounds
+          float* gcol = dst + ue * 2 + s_im;  // G[w][ue] at gcol[w * 128]
+          if (cc < 4) {
+#pragma unroll
+            for (int v = 0; v < 16; ++v) {
+              const float mine = __uint_as_float(r[2 * v]);
+              const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[2 * v + 1]), 1);
+              gcol[(16 * cc + v) * 128] = fmaf(sg, po, mine);
+            }
+          } else {
+            float* ycol = gcol + 64 * 64 * 2;  // y_mrc[t][ue] at ycol[t * 128]
+#pragma unroll
+            for (int v = 0; v < 16; ++v) {
+              const float mine = __uint_as_float(r[2 * v]);
+              const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[2 * v + 1]), 1);
+              if (v < T) ycol[v * 128] = fmaf(sg, mine, po);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int v = 0; v < 16; ++v) {
           const float mine = __uint_as_float(r[2 * v]);
           const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(r[2 * v + 1]), 1);
-          const float val = s_im ? (po - mine) : (mine + po);
           if (ue < u) {
             if (cc < 4) {  // G[ue][w] stored as G[w][ue] = conj(G[ue][w])
               const int wc = 16 * cc + v;
-              if (wc < u) dst[((size_t)wc * u + ue) * 2 + s_im] = s_im ? -val : val;
+              if (wc < u) dst[((size_t)wc * u + ue) * 2 + s_im] = fmaf(sg, po, mine);
             } else if (v < T) {  // y_mrc[t = v][ue]
-              dst[((size_t)u * u + (size_t)v * u + ue) * 2 + s_im] = val;
+              dst[((size_t)u * u + (size_t)v * u + ue) * 2 + s_im] = fmaf(sg, mine, po);
             }
           }
         }

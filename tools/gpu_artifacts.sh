@@ -1,9 +1,9 @@
-# Round artifacts on one B200 (outputs in gpurun_out/r02/):
+# Round artifacts on one B200 (outputs in gpurun_out/$TAG/, TAG default r02):
 #   headline bench line (cfg2, full JSON), per-config bench lines, reference arm,
 #   launch list of the headline run, ncu --set full captures of the dominant
 #   kernel of cfg2 / cfg3-zf / cfg4-fd / cfg5-pd512 (each after a clean run).
 set -u
-O=gpurun_out/r02
+O=gpurun_out/${TAG:-r02}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
 timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err; tail -c 400 $O/bench_cfg2.json
@@ -26,6 +26,7 @@ cap() {  # name config kernel-regex skip
 cap cfg2 cfg2 tc2_kernel 4
 cap cfg3zf cfg3-zf tc2_kernel 4
 cap cfg4fd cfg4-fd stream_kernel 3
-cap cfg5pd512_stats cfg5-pd512 tc_kernel 3
-cap cfg5pd512_solve cfg5-pd512 stats_kernel 3
+cap cfg5pd512_stats cfg5-pd512 tcw_stats 3
+cap cfg5pd512_solve cfg5-pd512 ^stats_kernel 3
+cap cfg1 cfg1 tc2_kernel 4
 ls -la $O
