@@ -310,20 +310,19 @@ struct T2FdAcc {
   int* st;      // status of the item (first failing cluster's code)
 };
 
-// Gauss-Jordan steps per unrolled frame of t2_solve_pair (register rotation
-// by T2_GJU after each frame)
-#ifndef T2_GJU
-#define T2_GJU 4
-#endif
-static_assert(16 % T2_GJU == 0, "frame must divide 16");
+// Register rotation by GJU after each unrolled frame of GJU Gauss-Jordan
+// steps in t2_solve_pair (GJU = 4 for PD, 8 for the solver-bound FD kernels:
+// measured 2.7 % faster there)
+template <int GJU>
 __device__ __forceinline__ void t2_rotate(float2 (&m)[16]) {
-  float2 t[T2_GJU];
+  static_assert(16 % GJU == 0, "frame must divide 16");
+  float2 t[GJU];
 #pragma unroll
-  for (int i = 0; i < T2_GJU; ++i) t[i] = m[i];
+  for (int i = 0; i < GJU; ++i) t[i] = m[i];
 #pragma unroll
-  for (int i = 0; i < 16 - T2_GJU; ++i) m[i] = m[i + T2_GJU];
+  for (int i = 0; i < 16 - GJU; ++i) m[i] = m[i + GJU];
 #pragma unroll
-  for (int i = 0; i < T2_GJU; ++i) m[16 - T2_GJU + i] = t[i];
+  for (int i = 0; i < GJU; ++i) m[16 - GJU + i] = t[i];
 }
 
 // Two units per warp, one per half-warp: MRC / ZF / L-MMSE (equalize.py:130-
@@ -333,9 +332,9 @@ __device__ __forceinline__ void t2_rotate(float2 (&m)[16]) {
 // written as the branch-free rank-1 update  m_ij -= c_i r_j  with
 //   c_i = M_ik (i != k), c_k = p - 1;   r_j = M_kj / p (j != k), r_k = 1 + 1/p
 // (which yields M_kj/p on the pivot row, -M_ik/p on the pivot column, 1/p on
-// the pivot).  r_j is the lane's own element; the pivot column is published
-// by lane k through a double-buffered shared-memory column and read back as
-// broadcasts.  A = M^-1 is Hermitian, so lane j also holds row j of A
+// the pivot).  r_j is the lane's own element; the pivot column comes from
+// lane k's registers by shuffles (measured 2.6 % faster on cfg2 than a
+// shared-memory column, whose round trip sat on the pivot chain).  A = M^-1 is Hermitian, so lane j also holds row j of A
 // (conjugated): x_t[j] = sum_i conj(A_ij) y_t[i], sigma2 = N0 A_jj,
 // c = 1 - rho A_jj, unbiased z / c and N0 A_jj / c.  MRC: d = G_jj, z = y / d,
 // sigma2 = N0/d + Es sum_{v != j} |G_jv|^2 / d^2.  A pivot below 8 u eps of
@@ -343,7 +342,7 @@ __device__ __forceinline__ void t2_rotate(float2 (&m)[16]) {
 // zpotrf's "not positive definite").  PD writes x-hat / decisions / sigma2 /
 // gain / status; FD adds w z, w, 1/sigma2 (w = 1/max(sigma2, 1e-15), MRC: the
 // Gram diagonal, fusion.py:96-105,149-151) to the half-warp's sums in `acc`.
-template <bool FD>
+template <bool FD, int GJU = FD ? 8 : 4>
 __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
                               const bool* valid, int lane, const T2FdAcc* acc = nullptr) {
   const int h = lane >> 4, j = lane & 15;
@@ -355,7 +354,6 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   const float n0h = h ? n0[1] : n0[0];
   const float2* G = h ? w[1].G : w[0].G;
   const float2* Z = h ? w[1].Z : w[0].Z;
-  float2* colb = h ? w[1].W : w[0].W;  // [2][16] pivot columns (double-buffered)
   const float rho = lmmse ? n0h / p.es : 0.f;
   float2 m[16];
   float dg = 1.f;
@@ -376,41 +374,34 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   if (!mrc) {
     const float tolf = 8.f * (float)u * FLT_EPSILON;
     // Rotating register order: at step k the lane's row-k element is
-    // m[k % T2_GJU] of the current frame, and after every T2_GJU steps the
-    // registers rotate by T2_GJU, so all indices stay static within an
+    // m[k % GJU] of the current frame, and after every GJU steps the
+    // registers rotate by GJU, so all indices stay static within an
     // unrolled frame; the pivot column is published and read in the same
     // frame.  Padded steps (k >= u) are identity pivots and no-ops: whole
     // frames of them are skipped and replaced by the bare register rotation
     // that restores the order.
 #pragma unroll 1
-    for (int k0 = 0; k0 < 16; k0 += T2_GJU) {
+    for (int k0 = 0; k0 < 16; k0 += GJU) {
       if (k0 >= u) {
-        t2_rotate(m);
+        t2_rotate<GJU>(m);
         continue;
       }
 #pragma unroll
-      for (int kk = 0; kk < T2_GJU; ++kk) {
+      for (int kk = 0; kk < GJU; ++kk) {
         const int k = k0 + kk;
-        float2* cb = colb + (kk & 1) * 16;
-        if (j == k) {  // publish the pivot column (a failed pivot is replaced by 1)
-          float2 pk = m[kk];
-          if (act && k < u && !(pk.x > tolf * dg)) {
-            bad = true;
-            pk = make_float2(1.f, 0.f);
-          }
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const float2 a0 = (i == kk) ? pk : m[i], a1 = (i + 1 == kk) ? pk : m[i + 1];
-            *reinterpret_cast<float4*>(cb + i) = make_float4(a0.x, a0.y, a1.x, a1.y);
-          }
-        }
-        __syncwarp();
         float2 cc[16];
+        // the pivot column straight from the pivot lane's registers (shuffles,
+        // no shared-memory round trip); every lane applies the singular-pivot
+        // replacement itself with the pivot lane's original diagonal
+        {
+          const int src = (lane & 16) | k;
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float4 v = *reinterpret_cast<const float4*>(cb + i);
-          cc[i] = make_float2(v.x, v.y);
-          cc[i + 1] = make_float2(v.z, v.w);
+          for (int i = 0; i < 16; ++i) cc[i] = shfl2(m[i], src);
+          const float dgk = __shfl_sync(0xffffffffu, dg, src);
+          if (act && k < u && !(cc[kk].x > tolf * dgk)) {
+            if (j == k) bad = true;
+            cc[kk] = make_float2(1.f, 0.f);
+          }
         }
         const float pv = cc[kk].x;
         const float rp = __frcp_rn(pv);
@@ -419,7 +410,7 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
 #pragma unroll
         for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
       }
-      t2_rotate(m);
+      t2_rotate<GJU>(m);
     }
   }
   // per-lane scalars: A_jj (ZF / L-MMSE) or d = G_jj and the off-diagonal
