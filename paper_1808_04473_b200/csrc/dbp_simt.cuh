@@ -332,6 +332,15 @@ __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqPar
   for (int64_t n = blockIdx.x; n < p.n_items; n += gridDim.x) {
     reset_flags(w, tm);
     const float2* src = p.stats_in + n * rec;
+    if (tid == 0 && n + gridDim.x < p.n_items) {  // this CTA's next record into L2 while this one solves
+      const char* nx = reinterpret_cast<const char*>(p.stats_in + (n + gridDim.x) * rec);
+      const uint32_t bytes = (uint32_t)(rec * sizeof(float2));
+      for (uint32_t o = 0; o < bytes; o += 32768) {
+        const uint32_t len = min(32768u, bytes - o) & ~15u;
+        if (len && !(reinterpret_cast<uintptr_t>(nx + o) & 15))
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + o), "r"(len) : "memory");
+      }
+    }
     if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_in) & 15)) {  // float4 pairs, shifts instead of divisions
       constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
       const float4* s4 = reinterpret_cast<const float4*>(src);  // rec is even: 16-byte aligned
