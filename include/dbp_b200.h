@@ -95,7 +95,8 @@ int dbp_last_kernel(void);
 #define DBP_OPT_SIMT_NS 5     /* SIMT kernel: stage ring depth */
 #define DBP_OPT_NO_WIDE 6     /* U = 64: SIMT statistics instead of the tensor cores */
 #define DBP_OPT_T2_NSPLIT 7   /* split-bf16 kernel: bf16 parts per operand (2, 3) */
-#define DBP_OPT_COUNT 8
+#define DBP_OPT_T2_QUAD 8     /* split-bf16 kernel, u <= 8: 2 = two units per solver pass instead of four */
+#define DBP_OPT_COUNT 9
 int dbp_set_option(int key, int value);
 int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_bytes);
 

@@ -33,7 +33,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-template <int MODE, int NSPLIT>
+template <int MODE, int NSPLIT, int QUAD = 0>
 static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm, const CUtensorMap& ym,
                            cudaStream_t st) {
   const bool fd = MODE == T2_FD;
@@ -42,7 +42,7 @@ static int launch_tc2_mode(EqParams& p, const Tc2Geom& g, const CUtensorMap& hm,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (L.total > smem_max) return 1;
-  auto kern = tc2_kernel<MODE, NSPLIT>;
+  auto kern = tc2_kernel<MODE, NSPLIT, QUAD>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   const int64_t grid = std::min<int64_t>(g.G_tot / g.upi, (int64_t)sm_count());  // CTAs own whole item blocks
@@ -103,6 +103,10 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   g.hbytes = 4 * 32 * 2 * p.us * 4;
   g.ybox = 4 * p.T * T2_YROW * 4;
   g.lean = 1;
+  // u <= 8: four units per solver pass (PD, or FD whose items fit a pass);
+  // option t2_quad = 2 forces the two-unit solver (tests)
+  g.quad = (p.u <= 8 && p.us <= 8 && opt(DBP_OPT_T2_QUAD) != 2 &&
+            (p.arch == ARCH_PD || (p.arch == ARCH_FD && (upi == 1 || upi == 2 || upi == 4)))) ? 1 : 0;
   const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : (p.arch == ARCH_PD) ? 2 : 3;
   if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
   const int raw = g.hbytes + g.ybox;
@@ -145,6 +149,10 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   }
   if (p.arch == ARCH_STATS) return nsplit == 2 ? launch_tc2_mode<T2_STATS, 2>(p, g, hm, ym, st)
                                                : launch_tc2_mode<T2_STATS, 3>(p, g, hm, ym, st);
+  if (g.quad) {
+    if (fdm) return nsplit == 2 ? launch_tc2_mode<T2_FD, 2, 1>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3, 1>(p, g, hm, ym, st);
+    return nsplit == 2 ? launch_tc2_mode<T2_PD, 2, 1>(p, g, hm, ym, st) : launch_tc2_mode<T2_PD, 3, 1>(p, g, hm, ym, st);
+  }
   if (fdm) return nsplit == 2 ? launch_tc2_mode<T2_FD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_FD, 3>(p, g, hm, ym, st);
   return nsplit == 2 ? launch_tc2_mode<T2_PD, 2>(p, g, hm, ym, st) : launch_tc2_mode<T2_PD, 3>(p, g, hm, ym, st);
 }

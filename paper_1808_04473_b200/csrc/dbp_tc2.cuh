@@ -118,6 +118,7 @@ struct Tc2Geom {
   int hbytes;   // bytes of the H box (4 units x 32 x 2us floats)
   int ybox;     // bytes of the Y box (4 items x T rows x 68 floats)
   int lean;     // compact solver work areas (G, y_mrc, pivot columns, flags)
+  int quad;     // u <= 8: four units per solver warp pass (t2_solve_quad)
   int64_t n_items;
   int64_t G_tot;  // groups in the launch = ceil(n_items / 4) * upi
 };
@@ -145,25 +146,25 @@ __host__ __device__ inline Tc2Layout make_tc2_layout(const Tc2Geom& g, int TP, i
   o += g.NS * g.stage_bytes;
   L.work = o;
   L.w = make_work_layout(0, 16, TP, C, false, false);
-  {  // compact work area: G, y_mrc, the pivot-column buffers, status flags
-    const int LD = 16 + 2;
+  const int UPW = g.quad ? 8 : 16;  // unit width of a work area
+  {  // compact work area: G, y_mrc, status flags
+    const int LD = UPW + 2;
     int q = 0;
     L.w.G = q;
-    q += 16 * LD * 8;
+    q += UPW * LD * 8;
     L.w.Z = q;
     q += TP * LD * 8;
     L.w.W = q;
-    q += 32 * 8;
     L.w.flags = q;
     L.w.X = L.w.Sv = L.w.Vv = L.w.Fb = L.w.gb = L.w.num = L.w.Z;
     L.w.phi = L.w.coef = L.w.s2 = L.w.gn = L.w.dg = L.w.den = L.w.harm = L.w.wbuf = L.w.Z;
     L.w.total = align_up(q + 16, 128);
   }
-  // +16 bytes: the two half-warps' pivot-column buffers start 4 banks apart
+  // +16 bytes: neighbouring work areas start 4 banks apart
   L.work_stride = L.w.total + 16;
-  o += T2_NWORK * L.work_stride;
+  o += (g.quad ? 2 : 1) * T2_NWORK * L.work_stride;
   L.fdacc = o;
-  L.fdacc_stride = fd ? t2_fdacc_bytes(g.T, C) : 0;
+  L.fdacc_stride = (fd && !g.quad) ? t2_fdacc_bytes(g.T, C) : 0;
   o += T2_NSOLV * L.fdacc_stride;
   L.total = align_up(o, 128);
   return L;
@@ -241,6 +242,15 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) 
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns (no wait)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
 }
@@ -510,6 +520,154 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   }
 }
 
+// Four units per warp, one per quarter-warp, for u <= 8: the same solves as
+// t2_solve_pair on 8 x 8 matrices (lane (qq, j) = (lane / 8, lane % 8) owns
+// column j of unit qq, eight rows in registers; pivot columns by shuffles
+// within the quarter).  PD writes every item's outputs; FD (units of one item
+// in consecutive quarters, upi = 1, 2 or 4 clusters) fuses the item's
+// clusters with xor-shuffles across its quarters (fusion.py:96-124) and its
+// first quarter writes x-hat / decisions / sigma2, every quarter its nu.
+template <bool FD>
+__device__ void t2_solve_quad(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
+                              const bool* valid, int lane, int upi) {
+  const int qq = lane >> 3, j = lane & 7;
+  const int u = p.u, T = p.T, LD = w[0].LD;
+  const bool lmmse = p.kind == EQ_LMMSE, mrc = p.kind == EQ_MRC;
+  bool act = valid[0];
+  int64_t nq = n[0];
+  int cq = c[0];
+  float n0q = n0[0];
+  const float2* G = w[0].G;
+  const float2* Z = w[0].Z;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (qq == k) {
+      act = valid[k];
+      nq = n[k];
+      cq = c[k];
+      n0q = n0[k];
+      G = w[k].G;
+      Z = w[k].Z;
+    }
+  const float rho = lmmse ? n0q / p.es : 0.f;
+  float2 m[8];
+  float dg = 1.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding (u < 8, idle quarter): identity
+    if (act && i < u && j < u) {
+      v = G[i * LD + j];
+      if (i == j) {
+        v.x += rho;
+        v.y = 0.f;
+        dg = v.x;
+      }
+    }
+    m[i] = v;
+  }
+  bool bad = false;
+  if (!mrc) {
+    const float tolf = 8.f * (float)u * FLT_EPSILON;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= u) break;  // padded steps are identity pivots (u is warp-uniform)
+      const int src = (lane & 24) | k;
+      float2 cc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cc[i] = shfl2(m[i], src);
+      const float dgk = __shfl_sync(0xffffffffu, dg, src);
+      if (act && !(cc[k].x > tolf * dgk)) {
+        if (j == k) bad = true;
+        cc[k] = make_float2(1.f, 0.f);
+      }
+      const float pv = cc[k].x;
+      const float rp = __frcp_rn(pv);
+      const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[k], rp);
+      cc[k] = make_float2(pv - 1.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c_fms(m[i], cc[i], r);
+    }
+  }
+  float ajj = 0.f, off = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i == j) ajj = m[i].x;
+    else if (mrc && i < u) off += c_abs2(m[i]);
+  }
+  const bool live = act && j < u;
+  if (mrc && live && !(ajj > 0.f)) bad = true;  // MRC: Gram diagonal <= 0
+  const bool unb = lmmse && (FD || p.unbias);
+  const float cgain = 1.f - rho * ajj;
+  const float sc = mrc ? __frcp_rn(ajj) : unb ? __frcp_rn(cgain) : 1.f;
+  const bool badc = live && unb && !(cgain > 0.f);
+  const unsigned bm = __ballot_sync(0xffffffffu, bad || badc);
+  float s2;
+  if (mrc) {
+    const float rd = __frcp_rn(ajj);
+    s2 = n0q * rd + p.es * off * rd * rd;
+  } else {
+    const float nv = n0q * ajj;
+    s2 = (p.kind == EQ_ZF) ? nv : (unb ? nv / cgain : nv);
+  }
+  const float inv = live ? 1.f / fmaxf(s2, VAR_FLOOR) : 0.f;
+  const float wgt = live ? (mrc ? ajj : inv) : 0.f;
+  const unsigned bv = __ballot_sync(0xffffffffu, FD && !mrc && live && !(s2 > 0.f));
+  // FD: sums over the item's quarters (consecutive, upi of them)
+  auto fuse = [&](float v) {
+    if (FD && upi >= 2) v += __shfl_xor_sync(0xffffffffu, v, 8);
+    if (FD && upi == 4) v += __shfl_xor_sync(0xffffffffu, v, 16);
+    return v;
+  };
+  const float den = fuse(wgt), harm = fuse(inv);
+  const bool lead = !FD || cq == 0;  // the quarter that writes the item's outputs
+  for (int t = 0; t < T; ++t) {
+    const float2* z = Z + t * LD;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+    if (live) {
+      if (mrc) {
+        a0 = z[j];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          if (i >= u) break;
+          const float4 y = *reinterpret_cast<const float4*>(z + i);  // y_t[i] beyond u is zero
+          c_fma_conj(a0, m[i], make_float2(y.x, y.y));
+          c_fma_conj(a1, m[i + 1], make_float2(y.z, y.w));
+        }
+      }
+    }
+    float2 x = c_scale(c_add(a0, a1), sc);
+    if constexpr (FD) {
+      const float2 xw = c_scale(x, wgt);
+      x = c_scale(make_float2(fuse(xw.x), fuse(xw.y)), 1.f / den);
+    }
+    if (live && lead) {
+      const size_t o = ((size_t)nq * T + t) * u + j;
+      p.xhat[o] = x;
+      if (p.dec) p.dec[o] = (uint8_t)t2_slice(x, p.cp);
+    }
+  }
+  if (live) {
+    if constexpr (FD) {
+      if (lead) p.sigma2[(size_t)nq * u + j] = 1.f / harm;
+      if (p.nu) p.nu[((size_t)nq * p.C + cq) * u + j] = wgt / den;
+    } else {
+      p.sigma2[(size_t)nq * u + j] = s2;
+      if (p.gain && (lmmse || mrc)) p.gain[(size_t)nq * u + j] = mrc ? ajj : cgain;
+    }
+  }
+  if (act && lead && j == 0) {
+    int code = 0;  // FD: the first failing cluster's code (clusters in quarter order)
+    for (int e = 0; e < (FD ? upi : 1); ++e) {
+      const int qe = qq + e;
+      const int ce = ((bm >> (8 * qe)) & 0xffu) ? ST_SINGULAR : ((bv >> (8 * qe)) & 0xffu) ? ST_BADVAR : 0;
+      if (!code) code = ce;
+    }
+    p.status[nq] = code;
+    if (p.iters) p.iters[nq] = 0;
+  }
+}
+
 // The item's FD fusion (fusion.py:108-124, 141-154) from the two half-warps'
 // sums: x = sum_c w_c z_c / sum_c w_c, sigma2 = 1 / sum_c 1/max(sigma2_c,
 // 1e-15), nu_c = w_c / sum w; or the raw sums for a cross-GPU reduction
@@ -605,7 +763,7 @@ __global__ void __launch_bounds__(32 * T2S_WARPS) t2_stats_solve_kernel(const __
   }
 }
 
-template <int MODE, int NSPLIT>
+template <int MODE, int NSPLIT, int QUAD = 0>
 // register cap: a warp lives on one of the 4 SM sub-partitions (16K registers
 // each), which hold ceil(warps / 4) warps
 __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
@@ -845,6 +1003,75 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
     const int sset = sv >> 2;  // = the accumulator this warp reads
     const int q = warp & 3;    // TMEM lane quarter this warp may access
     const Team<32, -1> tm{lane};
+    if constexpr (QUAD) {
+      // u <= 8: four units per pass (consecutive in the warp's unit sequence;
+      // FD items, upi | 4 units, never straddle a pass), one per quarter-warp
+      Work w4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        WorkLayout wl = L.w;
+        const int base = L.work + (4 * sv + k) * L.work_stride;
+        wl.G += base; wl.Z += base; wl.X += base; wl.W += base; wl.Sv += base; wl.Vv += base; wl.Fb += base;
+        wl.gb += base; wl.num += base; wl.phi += base; wl.coef += base; wl.s2 += base; wl.gn += base;
+        wl.dg += base; wl.den += base; wl.harm += base; wl.wbuf += base; wl.flags += base;
+        w4[k] = make_work(smem, wl, 8);
+      }
+      const int u = p.u, T = p.T, LD = w4[0].LD, upi = g.upi;
+      const int uh = lane >> 1, s_im = lane & 1;
+      const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+      const int units = ((nblocks - sset + 1) / 2) * upi;
+      int use = 0;
+      for (int k0 = 0; k0 < units; k0 += 4) {
+        int64_t n[4];
+        int c[4];
+        float n0[4];
+        bool valid[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          valid[k] = false;
+          n[k] = 0;
+          c[k] = 0;
+          n0[k] = 0.f;
+          const int uix = k0 + k;
+          if (uix >= units) continue;
+          const int lb = sset + 2 * (uix / upi);
+          c[k] = uix - (uix / upi) * upi;
+          n[k] = (b_first + lb) * 4 + q;
+          valid[k] = n[k] < g.n_items;
+          if (valid[k]) n0[k] = item_n0(p, n[k]);
+          T2_WAITR(&acc_full[sset], (uint32_t)(use & 1), 1, 8);
+          ++use;
+          tc_fence_after();
+          uint32_t gr[16], yr[32];
+          tmem_ld16_nw(tq + (uint32_t)(256 * sset + 32 * q), gr);
+          tmem_ld32_nw(tq + (uint32_t)(256 * sset + 128 + 32 * q), yr);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[sset]);
+          if (!valid[k]) continue;
+          float* Gf = reinterpret_cast<float*>(w4[k].G);
+          float* Zf = reinterpret_cast<float*>(w4[k].Z);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const float mine = __uint_as_float(gr[2 * v]);
+            const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(gr[2 * v + 1]), 1);
+            const float val = s_im ? (po - mine) : (mine + po);
+            if (uh < u && v < u) Gf[(v * LD + uh) * 2 + s_im] = s_im ? -val : val;  // G[v][uh] = conj(G[uh][v])
+          }
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const float mine = __uint_as_float(yr[2 * t]);
+            const float po = __shfl_xor_sync(0xffffffffu, __uint_as_float(yr[2 * t + 1]), 1);
+            const float val = s_im ? (po - mine) : (mine + po);
+            if (t < T && uh < 8) Zf[(t * LD + uh) * 2 + s_im] = (uh < u) ? val : 0.f;
+          }
+        }
+        __syncwarp();
+        t2_solve_quad<MODE == T2_FD>(w4, p, n, c, n0, valid, lane, upi);
+        __syncwarp();
+      }
+    } else {
     Work w[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -954,6 +1181,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
       }
       __syncwarp();
     }
+    }  // !QUAD
   }
 #ifdef DBP_STUDY
   if (p.dbg && lane == 0) {

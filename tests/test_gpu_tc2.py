@@ -136,3 +136,36 @@ def test_stats_solve_symbol_counts(kind, t):
             z, s2, _ = O.linear_equalize(kind, g, m, n0)
             assert normwise_rel(zi[tt], z) < XHAT_TOL, (i, tt)
             assert entry_rel(s2i[0], s2) < SIGMA2_TOL, (i, tt)
+
+
+@pytest.mark.parametrize("arch,kind,n,b,c,u,t", [
+    ("fd", "lmmse", 9, 64, 2, 8, 14),   # cfg1 shape: two items per pass, odd item count
+    ("fd", "zf", 6, 128, 4, 8, 14),     # four clusters: one item per pass
+    ("fd", "mrc", 5, 64, 1, 8, 7),      # one cluster: four items per pass
+    ("fd", "lmmse", 7, 96, 3, 8, 14),   # three clusters: the two-unit solver (items would straddle a pass)
+    ("pd", "lmmse", 11, 64, 2, 8, 14),
+    ("pd", "zf", 6, 96, 3, 5, 3),       # odd u
+    ("pd", "mrc", 3, 64, 2, 8, 16),
+])
+def test_quad_solver_matches_pair_and_oracle(arch, kind, n, b, c, u, t):
+    """u <= 8: four units per solver pass (t2_solve_quad) against the two-unit
+    solver (option t2_quad = 2) and the float64 oracle."""
+    H, Y, const, n0 = _inputs(n, b, u, t, 4, 5 * n + b + u)
+    counts = [b // c] * c
+    q = dbp.detect(arch, kind, H, Y, n0, counts, const)
+    assert _lib.lib().dbp_last_kernel() == _lib.KERNEL_TC_BF16
+    with _lib.options(t2_quad=2):
+        pr = dbp.detect(arch, kind, H, Y, n0, counts, const)
+    assert normwise_rel(q.xhat, pr.xhat) < 2e-6, normwise_rel(q.xhat, pr.xhat)
+    offs = [0] + list(np.cumsum(counts))
+    ref = O.run_batch(arch, kind, H.astype(complex), Y.astype(complex), offs, n0, 1.0, const.symbols)
+    assert normwise_rel(q.xhat, ref["z"]) < XHAT_TOL
+    s2 = np.broadcast_to(q.sigma2[:, None, :], ref["sigma2"].shape)
+    assert entry_rel(s2, ref["sigma2"]) < SIGMA2_TOL
+    nbad, ntot, at_boundary = check_decisions(q.decisions, ref["dec"], ref["z"], q.xhat, const.pam_levels)
+    assert at_boundary and nbad <= 1, nbad
+    if arch == "fd":
+        nu = np.broadcast_to(q.nu[:, None], ref["nu"].shape)
+        assert entry_rel(nu, ref["nu"]) < NU_TOL
+    else:
+        assert np.array_equal(q.decisions, pr.decisions) or nbad <= 1
