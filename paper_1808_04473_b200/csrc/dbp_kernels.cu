@@ -519,6 +519,49 @@ static int fill_const(ConstParams& cp, const float* levels, int L, const float* 
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
 static int dispatch_stats(EqParams& p, cudaStream_t st);
 
+// FD, 32 < u <= 64, linear: per-cluster statistics {G_c, y_c} on the tensor
+// cores (wide split-bf16 kernel, 3 parts: the per-cluster Grams of B_c = U
+// antennas are ill-conditioned), then per item the cluster solves and their
+// fusion in stats_kernel (look-ahead blocked Gauss-Jordan, two CTAs per SM).
+// In chunks of items: the per-cluster records are as large as the input.
+// Returns 1 when the geometry is not covered.
+static int fd_wide(EqParams& p, cudaStream_t st) {
+  const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
+  const size_t per_item = (size_t)p.C * rec * sizeof(float2);
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(((size_t)3 << 30) / per_item));  // ~3 GB of records
+  if (opt(DBP_OPT_WIDE_CHUNK) > 0) chunk = opt(DBP_OPT_WIDE_CHUNK);                 // tests
+  if (p.n0_dev) chunk = std::max<int64_t>(1, chunk / p.n0_group) * p.n0_group;  // n0 runs stay whole
+  chunk = std::min<int64_t>(chunk, p.n_items);
+  float2* stats = static_cast<float2*>(stream_scratch(st, (size_t)chunk * per_item));
+  if (!stats) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
+  const int u = p.u, T = p.T;
+  for (int64_t i0 = 0; i0 < p.n_items; i0 += chunk) {
+    const int64_t len = std::min<int64_t>(chunk, p.n_items - i0);
+    EqParams q = p;
+    q.n_items = len;
+    q.H = p.H + (size_t)i0 * p.B * p.us;
+    q.Y = p.Y + (size_t)i0 * T * p.B;
+    q.xhat = p.xhat + (size_t)i0 * T * u;
+    if (p.dec) q.dec = p.dec + (size_t)i0 * T * u;
+    q.sigma2 = p.sigma2 + (size_t)i0 * u;
+    if (p.nu) q.nu = p.nu + (size_t)i0 * p.C * u;
+    if (p.gain) q.gain = p.gain + (size_t)i0 * u;
+    q.status = p.status + i0;
+    if (p.iters) q.iters = p.iters + i0;
+    if (p.n0_dev) q.n0_dev = p.n0_dev + i0 / p.n0_group;
+    EqParams s = q;
+    s.arch = ARCH_STATS;
+    s.sum_clusters = 0;
+    s.stats_out = stats;
+    int rc = launch_tcw(s, st, 3);
+    if (rc) return rc;  // 1: geometry not covered (the same for every chunk)
+    q.stats_in = stats;
+    rc = launch_stats_up(64, q, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 static int dispatch_stream(EqParams& p, cudaStream_t st) {
   p.g_hermitian = 1;  // the streaming kernels build G themselves (full Hermitian matrix)
   const int pol = opt(DBP_OPT_KERNEL);
@@ -543,6 +586,12 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
     p.NS = up <= 16 ? 4 : 3;
+  }
+  if (!force_simt && up == 64 && p.arch == ARCH_FD && p.kind != EQ_LAMA && !opt(DBP_OPT_NO_WIDE) &&
+      pol != DBP_KERNEL_TC_TF32) {
+    const int rc = fd_wide(p, st);
+    if (rc == 0) g_last_kernel = DBP_KERNEL_TC_BF16;
+    if (rc <= 0) return rc;
   }
   // U = 64: statistics {G, y_mrc} on the tensor cores (wide layout); PD
   // linear equalization then runs its solves in stats_kernel on them.  Not

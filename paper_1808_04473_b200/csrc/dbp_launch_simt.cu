@@ -56,7 +56,8 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
 template <int UP, int NT>
 static int launch_stats(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
-  const WorkLayout L = make_work_layout(0, UP, p.TP, 1, lama, false);
+  const bool fd = p.arch == ARCH_FD;
+  const WorkLayout L = make_work_layout(0, UP, p.TP, fd ? p.C : 1, lama, fd);
   auto kern = stats_kernel<UP, NT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");

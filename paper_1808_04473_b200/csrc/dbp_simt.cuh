@@ -317,45 +317,55 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 }
 
 // Equalization from precomputed statistics (PD central node after the
-// reduce-scatter; linear_equalize / lama_equalize API).
+// reduce-scatter; linear_equalize / lama_equalize API; and FD at U = 64, where
+// the records are the per-cluster statistics [n][C] of the wide tensor-core
+// kernel and each item's clusters are solved and fused in order).
 template <int UP, int NT>
 __global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
   const bool lama = p.kind == EQ_LAMA;
-  const WorkLayout L = make_work_layout(0, UP, p.TP, 1, lama, false);
+  const bool fd = p.arch == ARCH_FD;
+  const int ncl = fd ? p.C : 1;
+  const WorkLayout L = make_work_layout(0, UP, p.TP, ncl, lama, fd);
   const Work w = make_work(smem, L, UP);
   const Team<NT, 0> tm{tid};
   const int u = p.u, T = p.T;
   const size_t rec = (size_t)u * u + (size_t)T * u;
+  const int64_t nrec = p.n_items * ncl;
   int cl_first = 1;
   for (int64_t n = blockIdx.x; n < p.n_items; n += gridDim.x) {
     reset_flags(w, tm);
-    const float2* src = p.stats_in + n * rec;
-    if (tid == 0 && n + gridDim.x < p.n_items) {  // this CTA's next record into L2 while this one solves
-      const char* nx = reinterpret_cast<const char*>(p.stats_in + (n + gridDim.x) * rec);
-      const uint32_t bytes = (uint32_t)(rec * sizeof(float2));
-      for (uint32_t o = 0; o < bytes; o += 32768) {
-        const uint32_t len = min(32768u, bytes - o) & ~15u;
-        if (len && !(reinterpret_cast<uintptr_t>(nx + o) & 15))
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + o), "r"(len) : "memory");
+    for (int c = 0; c < ncl; ++c) {
+      const int64_t r = n * ncl + c;
+      const float2* src = p.stats_in + r * rec;
+      const int64_t rn = (c + 1 < ncl) ? r + 1 : (n + gridDim.x) * ncl;  // the record after this one
+      if (tid == 0 && rn < nrec) {  // into L2 while this one solves
+        const char* nx = reinterpret_cast<const char*>(p.stats_in + rn * rec);
+        const uint32_t bytes = (uint32_t)(rec * sizeof(float2));
+        for (uint32_t o = 0; o < bytes; o += 32768) {
+          const uint32_t len = min(32768u, bytes - o) & ~15u;
+          if (len && !(reinterpret_cast<uintptr_t>(nx + o) & 15))
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx + o), "r"(len) : "memory");
+        }
       }
-    }
-    if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_in) & 15)) {  // float4 pairs, shifts instead of divisions
-      constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
-      const float4* s4 = reinterpret_cast<const float4*>(src);  // rec is even: 16-byte aligned
-      for (int e = tid; e < (UP * UP + T * UP) / 2; e += NT) {
-        const int r = e >> SH, c = 2 * (e & (UP / 2 - 1));
-        float2* dst = (r < UP) ? w.G + r * w.LD + c : w.Z + (r - UP) * w.LD + c;
-        *reinterpret_cast<float4*>(dst) = s4[e];
+      if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_in) & 15)) {  // float4 pairs, shifts instead of divisions
+        constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
+        const float4* s4 = reinterpret_cast<const float4*>(src);  // rec is even: 16-byte aligned
+        for (int e = tid; e < (UP * UP + T * UP) / 2; e += NT) {
+          const int rr = e >> SH, cc = 2 * (e & (UP / 2 - 1));
+          float2* dst = (rr < UP) ? w.G + rr * w.LD + cc : w.Z + (rr - UP) * w.LD + cc;
+          *reinterpret_cast<float4*>(dst) = s4[e];
+        }
+      } else {
+        for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
+        for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
       }
-    } else {
-      for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
-      for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
+      __syncthreads();
+      // two CTAs per SM: look-ahead solve
+      unit_epilogue<UP, Team<NT, 0>, -1, true>(w, p, n, c, c + 1 == ncl, cl_first, tm);
+      __syncthreads();
     }
-    __syncthreads();
-    unit_epilogue<UP, Team<NT, 0>, -1, true>(w, p, n, 0, true, cl_first, tm);  // two CTAs per SM: look-ahead solve
-    __syncthreads();
   }
 }
 
