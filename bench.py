@@ -281,6 +281,9 @@ def reference_arm(args, wl, name):
 def kernel_name(kernel_id, wl, two_pass):
     up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
     tag = f"{wl['arch'].upper()}-{wl['kind']}"
+    if two_pass and wl["arch"] == "fd":
+        return ("dbp::tcw_stats_kernel (per-cluster split-bf16 statistics) + dbp::stats_kernel<64> (cluster "
+                "solves + fusion), per item chunk")
     if two_pass:
         if kernel_id == 3:
             return ("dbp::tcw_stats_kernel (split-bf16 tensor cores, one unit per M=128 x N=160 MMA) + "
@@ -408,8 +411,17 @@ def single_gpu(args, wl, name):
                 det.run(*copies[k % len(copies)], 0.0, n0_dev, W)
             torch.cuda.synchronize()
     kernel_id = _lib.lib().dbp_last_kernel()
-    two_pass = kernel_id in (2, 3) and wl["U"] == 64 and wl["arch"] == "pd"  # statistics + solve launches
-    launches = timed_launches * (2 if two_pass else 1)
+    # U = 64: statistics + solve launches (FD: per item chunk of ~3 GiB of
+    # per-cluster records, whole N0 runs of W items -- dispatch fd_wide)
+    two_pass = kernel_id in (2, 3) and wl["U"] == 64 and (wl["arch"] == "pd" or kernel_id == 3)
+    per_step = 1
+    if two_pass:
+        per_step = 2
+        if wl["arch"] == "fd":
+            rec_bytes = wl["C"] * (wl["U"] ** 2 + T * wl["U"]) * 8
+            chunk = max(1, (3 << 30) // rec_bytes // W) * W
+            per_step = 2 * math.ceil(n_items / chunk)
+    launches = timed_launches * per_step
     ms = elapsed_ms / args.steps
     bits = bits_per_step(wl)
     value = bits / (ms * 1e-3) / 1e9
@@ -491,7 +503,7 @@ def single_gpu(args, wl, name):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": kernel_name(kernel_id, wl, two_pass) + f", {2 if two_pass else 1} launch(es)/step"},
+                     "kernel": kernel_name(kernel_id, wl, two_pass) + f", {per_step} launch(es)/step"},
         "parity": parity,
         "cpu_baseline": cpu,
         "e2e": e2e,
