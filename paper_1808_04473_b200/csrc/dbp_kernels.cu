@@ -618,7 +618,8 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
       q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
       if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
       int kid = DBP_KERNEL_TC_BF16;
-      int rc = pol != DBP_KERNEL_TC_TF32 ? launch_tcw(q, st, 2) : 1;
+      // two bf16 parts for well-conditioned systems (B >= 4 u), else three (see launch_tc2)
+      int rc = pol != DBP_KERNEL_TC_TF32 ? launch_tcw(q, st, p.B >= 4 * p.u ? 2 : 3) : 1;
       if (rc == 1) {
         kid = DBP_KERNEL_TC_TF32;
         rc = launch_tc_up(64, q, st);
