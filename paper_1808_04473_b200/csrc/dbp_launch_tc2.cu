@@ -107,9 +107,13 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   // option t2_quad = 2 forces the two-unit solver (tests)
   g.quad = (p.u <= 8 && p.us <= 8 && opt(DBP_OPT_T2_QUAD) != 2 &&
             (p.arch == ARCH_PD || (p.arch == ARCH_FD && (upi == 1 || upi == 2 || upi == 4)))) ? 1 : 0;
-  // two bf16 parts only for well-conditioned PD systems (B >= 4 u: Gram
-  // condition number <= ~9); square-ish systems amplify the ~2^-17 product error
-  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : (p.arch == ARCH_PD && p.B >= 4 * p.u) ? 2 : 3;
+  // two bf16 parts (~2^-17 per product) where nothing amplifies them: MRC (no
+  // inverse) and well-conditioned PD systems (K >= 4 u antennas: Gram condition
+  // number <= ~9); three otherwise -- FD L-MMSE on cfg1 (B_c = 4 u) with two
+  // parts kept x-hat at 1.1e-5 but tripled the boundary decision flips past the
+  // 1e-5 rate bar -- and for the statistics API
+  const bool two = p.arch != ARCH_STATS && (p.kind == EQ_MRC || (p.arch == ARCH_PD && K >= 4 * p.u));
+  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : two ? 2 : 3;
   if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
   const int raw = g.hbytes + g.ybox;
   g.stage_bytes = align_up(std::max(raw, nsplit * T2_SPLIT_BYTES), 1024);

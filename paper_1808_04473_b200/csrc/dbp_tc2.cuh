@@ -320,39 +320,93 @@ struct T2FdAcc {
   int* st;      // status of the item (first failing cluster's code)
 };
 
-// Register rotation by GJU after each unrolled frame of GJU Gauss-Jordan
-// steps in t2_solve_pair (GJU = 4 for PD, 8 for the solver-bound FD kernels:
-// measured 2.7 % faster there)
-template <int GJU>
-__device__ __forceinline__ void t2_rotate(float2 (&m)[16]) {
-  static_assert(16 % GJU == 0, "frame must divide 16");
-  float2 t[GJU];
+
+// In-place Gauss-Jordan inverse of a 16 x 16 HPD unit on one half-warp, in
+// 4 x 4 blocks: lane (bi, bj) = ((lane / 4) % 4, lane % 4) of the half owns
+// rows 4 bi .., cols 4 bj .. .  The branch-free rank-1 step of t2_solve_pair,
+//   m_ij -= c_i r_j,  c_i = M_ik (i != k), c_k = p - 1;  r_j = M_kj / p (j != k), r_k = 1 + 1/p,
+// needs per lane only the pivot row's 4 entries of its columns and the pivot
+// column's 4 entries of its rows (shuffles from the two owning lanes): 18
+// shuffles per step for 16 complex updates, half the traffic of a column per
+// lane.  A pivot below 8 u eps of its original diagonal is singular (replaced
+// by 1 and flagged).  Padded rows / columns (>= u) are the identity and their
+// steps no-ops.  Reads G (+ rho on the diagonal) from, and writes A to, the
+// unit's work area (rows / cols < u).
+__device__ __forceinline__ void t2_gj2d(float2* Gw, int LD, int u, float rho, bool act, int lane, bool& bad) {
+  const int h16 = lane & 16, bi = (lane >> 2) & 3, bj = lane & 3;
+  float2 m[4][4];
+  float dgl[4];
 #pragma unroll
-  for (int i = 0; i < GJU; ++i) t[i] = m[i];
+  for (int r = 0; r < 4; ++r) {
 #pragma unroll
-  for (int i = 0; i < 16 - GJU; ++i) m[i] = m[i + GJU];
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * bi + r, jj = 4 * bj + c;
+      float2 v = make_float2(i == jj ? 1.f : 0.f, 0.f);
+      if (act && i < u && jj < u) {
+        v = Gw[i * LD + jj];
+        if (i == jj) {
+          v.x += rho;
+          v.y = 0.f;
+        }
+      }
+      m[r][c] = v;
+    }
+    dgl[r] = m[r][r].x;  // the original diagonal (meaningful on the diagonal lanes bi == bj)
+  }
+  const float tolf = 8.f * (float)u * FLT_EPSILON;
+  const int nkb = (u + 3) >> 2;
+#pragma unroll 1
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int srow = h16 | (kb << 2) | bj;  // owner of (row block kb, my column block)
+    const int scol = h16 | (bi << 2) | kb;  // owner of (my row block, column block kb)
+    const int spiv = h16 | (kb << 2) | kb;  // owner of the pivot block
 #pragma unroll
-  for (int i = 0; i < GJU; ++i) m[16 - GJU + i] = t[i];
+    for (int kr = 0; kr < 4; ++kr) {
+      float2 R[4], C[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) R[c] = shfl2(m[kr][c], srow);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) C[r] = shfl2(m[r][kr], scol);
+      float pv = __shfl_sync(0xffffffffu, m[kr][kr].x, spiv);
+      const float dgk = __shfl_sync(0xffffffffu, dgl[kr], spiv);
+      if (act && 4 * kb + kr < u && !(pv > tolf * dgk)) {
+        if (lane == spiv) bad = true;
+        pv = 1.f;
+      }
+      const float rp = __frcp_rn(pv);
+      float2 rr[4], cr[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) rr[c] = (bj == kb && c == kr) ? make_float2(1.f + rp, 0.f) : c_scale(R[c], rp);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cr[r] = (bi == kb && r == kr) ? make_float2(pv - 1.f, 0.f) : C[r];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) c_fms(m[r][c], cr[r], rr[c]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * bi + r, jj = 4 * bj + c;
+      if (act && i < u && jj < u) Gw[i * LD + jj] = m[r][c];
+    }
 }
 
 // Two units per warp, one per half-warp: MRC / ZF / L-MMSE (equalize.py:130-
-// 195).  Lane (h = lane / 16, j = lane % 16) owns column j of unit h's matrix
-// M = G + rho I (all 16 rows in registers).  ZF / L-MMSE: in-place
-// Gauss-Jordan inverse without pivoting (M is Hermitian positive definite),
-// written as the branch-free rank-1 update  m_ij -= c_i r_j  with
-//   c_i = M_ik (i != k), c_k = p - 1;   r_j = M_kj / p (j != k), r_k = 1 + 1/p
-// (which yields M_kj/p on the pivot row, -M_ik/p on the pivot column, 1/p on
-// the pivot).  r_j is the lane's own element; the pivot column comes from
-// lane k's registers by shuffles (measured 2.6 % faster on cfg2 than a
-// shared-memory column, whose round trip sat on the pivot chain).  A = M^-1 is Hermitian, so lane j also holds row j of A
-// (conjugated): x_t[j] = sum_i conj(A_ij) y_t[i], sigma2 = N0 A_jj,
+// 195).  ZF / L-MMSE: A = (G + rho I)^-1 in place by t2_gj2d (4 x 4 blocks
+// per lane; measured 3.4 % faster on cfg3-zf than a column per lane with the
+// pivot column shuffled in whole); then lane (h = lane / 16, j = lane % 16)
+// loads column j of A (all 16 rows).  A is Hermitian, so lane j also holds
+// row j of A (conjugated): x_t[j] = sum_i conj(A_ij) y_t[i], sigma2 = N0 A_jj,
 // c = 1 - rho A_jj, unbiased z / c and N0 A_jj / c.  MRC: d = G_jj, z = y / d,
 // sigma2 = N0/d + Es sum_{v != j} |G_jv|^2 / d^2.  A pivot below 8 u eps of
 // its original diagonal is SingularGramError (the fp32 counterpart of
 // zpotrf's "not positive definite").  PD writes x-hat / decisions / sigma2 /
 // gain / status; FD adds w z, w, 1/sigma2 (w = 1/max(sigma2, 1e-15), MRC: the
 // Gram diagonal, fusion.py:96-105,149-151) to the half-warp's sums in `acc`.
-template <bool FD, int GJU = FD ? 8 : 4>
+template <bool FD>
 __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
                               const bool* valid, int lane, const T2FdAcc* acc = nullptr) {
   const int h = lane >> 4, j = lane & 15;
@@ -362,66 +416,21 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
   const int64_t nh = h ? n[1] : n[0];
   const int ch = h ? c[1] : c[0];
   const float n0h = h ? n0[1] : n0[0];
-  const float2* G = h ? w[1].G : w[0].G;
+  float2* G = h ? w[1].G : w[0].G;
   const float2* Z = h ? w[1].Z : w[0].Z;
   const float rho = lmmse ? n0h / p.es : 0.f;
+  bool bad = false;
+  if (!mrc) {  // ZF / L-MMSE: A = (G + rho I)^-1 in place (4 x 4 blocks per lane)
+    t2_gj2d(G, LD, u, rho, act, lane, bad);
+    __syncwarp();
+  }
+  // lane j: column j of A (or of G for MRC), all 16 rows
   float2 m[16];
-  float dg = 1.f;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding (u < 16, idle half): identity
-    if (act && i < u && j < u) {
-      v = G[i * LD + j];
-      if (i == j) {
-        v.x += rho;
-        v.y = 0.f;
-        dg = v.x;
-      }
-    }
+    if (act && i < u && j < u) v = G[i * LD + j];
     m[i] = v;
-  }
-  bool bad = false;
-  if (!mrc) {
-    const float tolf = 8.f * (float)u * FLT_EPSILON;
-    // Rotating register order: at step k the lane's row-k element is
-    // m[k % GJU] of the current frame, and after every GJU steps the
-    // registers rotate by GJU, so all indices stay static within an
-    // unrolled frame; the pivot column is published and read in the same
-    // frame.  Padded steps (k >= u) are identity pivots and no-ops: whole
-    // frames of them are skipped and replaced by the bare register rotation
-    // that restores the order.
-#pragma unroll 1
-    for (int k0 = 0; k0 < 16; k0 += GJU) {
-      if (k0 >= u) {
-        t2_rotate<GJU>(m);
-        continue;
-      }
-#pragma unroll
-      for (int kk = 0; kk < GJU; ++kk) {
-        const int k = k0 + kk;
-        float2 cc[16];
-        // the pivot column straight from the pivot lane's registers (shuffles,
-        // no shared-memory round trip); every lane applies the singular-pivot
-        // replacement itself with the pivot lane's original diagonal
-        {
-          const int src = (lane & 16) | k;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) cc[i] = shfl2(m[i], src);
-          const float dgk = __shfl_sync(0xffffffffu, dg, src);
-          if (act && k < u && !(cc[kk].x > tolf * dgk)) {
-            if (j == k) bad = true;
-            cc[kk] = make_float2(1.f, 0.f);
-          }
-        }
-        const float pv = cc[kk].x;
-        const float rp = __frcp_rn(pv);
-        const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[kk], rp);
-        cc[kk] = make_float2(pv - 1.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) c_fms(m[i], cc[i], r);
-      }
-      t2_rotate<GJU>(m);
-    }
   }
   // per-lane scalars: A_jj (ZF / L-MMSE) or d = G_jj and the off-diagonal
   // row energy (MRC; row j = conj(column j))
