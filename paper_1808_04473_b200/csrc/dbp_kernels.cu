@@ -519,13 +519,13 @@ static int fill_const(ConstParams& cp, const float* levels, int L, const float* 
 // DBP_FORCE_SIMT=1 selects the SIMT kernel for every U (A/B measurements).
 static int dispatch_stats(EqParams& p, cudaStream_t st);
 
-// FD, 32 < u <= 64, linear: per-cluster statistics {G_c, y_c} on the tensor
-// cores (wide split-bf16 kernel, 3 parts: the per-cluster Grams of B_c = U
-// antennas are ill-conditioned), then per item the cluster solves and their
-// fusion in stats_kernel (look-ahead blocked Gauss-Jordan, two CTAs per SM).
+// FD through per-cluster statistics: {G_c, y_c} on the tensor cores (up = 64:
+// wide split-bf16 kernel, 3 parts -- the per-cluster Grams of B_c = U antennas
+// are ill-conditioned; up = 32: the 3xTF32 kernel), then per item the cluster
+// solves / LAMA recursions and their fusion in stats_kernel.
 // In chunks of items: the per-cluster records are as large as the input.
 // Returns 1 when the geometry is not covered.
-static int fd_wide(EqParams& p, cudaStream_t st) {
+static int fd_wide(EqParams& p, cudaStream_t st, int up = 64) {
   const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
   const size_t per_item = (size_t)p.C * rec * sizeof(float2);
   int64_t chunk = std::max<int64_t>(1, (int64_t)(((size_t)3 << 30) / per_item));  // ~3 GB of records
@@ -553,10 +553,10 @@ static int fd_wide(EqParams& p, cudaStream_t st) {
     s.arch = ARCH_STATS;
     s.sum_clusters = 0;
     s.stats_out = stats;
-    int rc = launch_tcw(s, st, 3);
+    int rc = up == 64 ? launch_tcw(s, st, 3) : launch_tc_up(up, s, st);
     if (rc) return rc;  // 1: geometry not covered (the same for every chunk)
     q.stats_in = stats;
-    rc = launch_stats_up(64, q, st);
+    rc = launch_stats_up(up, q, st);
     if (rc) return rc;
   }
   return 0;
@@ -586,6 +586,29 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
     if (rc <= 0) return rc;  // launched (0) or failed (< 0); 1 = use the SIMT kernel
     p.NS = up <= 16 ? 4 : 3;
+  }
+  // PD LAMA, 16 < u <= 32: the fused statistics on the tensor cores (3xTF32
+  // kernel), then the recursions in stats_kernel from them (the SIMT kernel's
+  // Gram mainloop was half of the step: cfg4-pd 3.72 -> 3.05 ms).  (FD LAMA
+  // the same way, per-cluster records through fd_wide, measured no faster:
+  // its step is the recursions.)
+  if (!force_simt && up == 32 && p.arch == ARCH_PD && p.kind == EQ_LAMA && !opt(DBP_OPT_NO_WIDE) &&
+      !p.tr_z) {
+    EqParams q = p;
+    q.arch = ARCH_STATS;
+    q.sum_clusters = 1;
+    const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
+    q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
+    if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
+    int rc = launch_tc_up(32, q, st);
+    if (rc < 0) return rc;
+    if (rc == 0) {
+      g_last_kernel = DBP_KERNEL_TC_TF32;
+      EqParams r = p;
+      r.stats_in = q.stats_out;
+      r.C = 1;
+      return launch_stats_up(32, r, st);
+    }
   }
   if (!force_simt && up == 64 && p.arch == ARCH_FD && p.kind != EQ_LAMA && !opt(DBP_OPT_NO_WIDE) &&
       pol != DBP_KERNEL_TC_TF32) {
