@@ -4,7 +4,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 CSRC := paper_1808_04473_b200/csrc
-SRCS := $(CSRC)/dbp_kernels.cu $(CSRC)/dbp_launch_tc2.cu $(CSRC)/dbp_launch_tc.cu $(CSRC)/dbp_launch_simt.cu $(CSRC)/dbp_comm.cu
+SRCS := $(CSRC)/dbp_kernels.cu $(CSRC)/dbp_launch_tc2.cu $(CSRC)/dbp_launch_tc.cu $(CSRC)/dbp_launch_simt.cu $(CSRC)/dbp_launch_lama.cu $(CSRC)/dbp_comm.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDR := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dbp_host.h include/dbp_b200.h
 LIB := paper_1808_04473_b200/libdbp_b200.so

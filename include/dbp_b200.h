@@ -97,7 +97,8 @@ int dbp_last_kernel(void);
 #define DBP_OPT_T2_NSPLIT 7   /* split-bf16 kernel: bf16 parts per operand (2, 3) */
 #define DBP_OPT_T2_QUAD 8     /* split-bf16 kernel, u <= 8: 2 = two units per solver pass instead of four */
 #define DBP_OPT_WIDE_CHUNK 9  /* FD, U = 64: items per statistics chunk (default ~3 GB of records) */
-#define DBP_OPT_COUNT 10
+#define DBP_OPT_LAMA_KERNEL 10 /* LAMA, u <= 32: 1 = the recursion inside the streaming / statistics kernels */
+#define DBP_OPT_COUNT 11
 int dbp_set_option(int key, int value);
 int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_bytes);
 

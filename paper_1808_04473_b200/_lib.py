@@ -26,7 +26,7 @@ ARCH_PD, ARCH_FD, ARCH_FD_PARTIAL = 1, 2, 3
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TC_TF32, KERNEL_TC_BF16 = 0, 1, 2, 3
 # dbp_set_option keys
 OPTIONS = {"kernel": 0, "tc_smax_kb": 1, "tc_ns": 2, "tc_pair": 3, "tc_nsolv": 4, "simt_ns": 5,
-           "no_wide": 6, "t2_nsplit": 7, "t2_quad": 8, "wide_chunk": 9}
+           "no_wide": 6, "t2_nsplit": 7, "t2_quad": 8, "wide_chunk": 9, "lama_kernel": 10}
 
 _vp, _fp, _i32p, _u8p = C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p
 _i64, _i, _f = C.c_int64, C.c_int, C.c_float

@@ -26,4 +26,6 @@ int launch_tcw(EqParams& p, cudaStream_t st, int nsplit_default = 3);
 int launch_tc_up(int up, EqParams& p, cudaStream_t st);
 int launch_stream_up(int up, EqParams& p, cudaStream_t st);
 int launch_stats_up(int up, EqParams& p, cudaStream_t st);
+// LAMA recursions from statistics records (u <= 32, PD / FD): 1 = not covered
+int launch_lama(EqParams& p, cudaStream_t st);
 }  // namespace dbp

@@ -501,7 +501,11 @@ static int fill_const(ConstParams& cp, const float* levels, int L, const float* 
   cp.L = L;
   cp.M = M;
   cp.es = es;
-  for (int l = 0; l < L; ++l) cp.levels[l] = levels[l];
+  for (int l = 0; l < L; ++l) {
+    cp.levels[l] = levels[l];
+    cp.lv2[l] = make_float2(levels[l], levels[l]);
+    cp.lq2[l] = make_float2(levels[l] * levels[l], levels[l] * levels[l]);
+  }
   for (int l = 0; l + 1 < L; ++l) cp.mids[l] = 0.5f * (levels[l] + levels[l + 1]);
   double mr = 0, mi = 0, e2 = 0;
   for (int k = 0; k < M; ++k) {
@@ -543,8 +547,9 @@ static int fd_wide(EqParams& p, cudaStream_t st, int up = 64) {
     q.Y = p.Y + (size_t)i0 * T * p.B;
     q.xhat = p.xhat + (size_t)i0 * T * u;
     if (p.dec) q.dec = p.dec + (size_t)i0 * T * u;
-    q.sigma2 = p.sigma2 + (size_t)i0 * u;
-    if (p.nu) q.nu = p.nu + (size_t)i0 * p.C * u;
+    const int wdim = p.kind == EQ_LAMA ? T : u;  // LAMA: sigma2 [n][T], nu [n][C][T]
+    q.sigma2 = p.sigma2 + (size_t)i0 * wdim;
+    if (p.nu) q.nu = p.nu + (size_t)i0 * p.C * wdim;
     if (p.gain) q.gain = p.gain + (size_t)i0 * u;
     q.status = p.status + i0;
     if (p.iters) q.iters = p.iters + i0;
@@ -556,7 +561,8 @@ static int fd_wide(EqParams& p, cudaStream_t st, int up = 64) {
     int rc = up == 64 ? launch_tcw(s, st, 3) : launch_tc_up(up, s, st);
     if (rc) return rc;  // 1: geometry not covered (the same for every chunk)
     q.stats_in = stats;
-    rc = launch_stats_up(up, q, st);
+    rc = launch_lama(q, st);  // LAMA (u <= 32): the register-resident recursion kernel
+    if (rc == 1) rc = launch_stats_up(up, q, st);
     if (rc) return rc;
   }
   return 0;
@@ -607,8 +613,18 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
       EqParams r = p;
       r.stats_in = q.stats_out;
       r.C = 1;
+      const int rl = launch_lama(r, st);
+      if (rl <= 0) return rl;
       return launch_stats_up(32, r, st);
     }
+  }
+  // FD LAMA, 16 < u <= 32: per-cluster statistics on the tensor cores, then
+  // the recursions and their fusion in lama_kernel (G in registers)
+  if (!force_simt && up == 32 && p.arch == ARCH_FD && p.kind == EQ_LAMA && !opt(DBP_OPT_NO_WIDE) && !p.tr_z &&
+      opt(DBP_OPT_LAMA_KERNEL) != 1) {
+    const int rc = fd_wide(p, st, 32);
+    if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
+    if (rc <= 0) return rc;
   }
   if (!force_simt && up == 64 && p.arch == ARCH_FD && p.kind != EQ_LAMA && !opt(DBP_OPT_NO_WIDE) &&
       pol != DBP_KERNEL_TC_TF32) {
@@ -663,8 +679,12 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
 }
 
 static int dispatch_stats(EqParams& p, cudaStream_t st) {
-  const int rc = launch_t2_stats_solve(p, st);  // u <= 16 ZF / L-MMSE: warp-pair solver
+  int rc = launch_t2_stats_solve(p, st);  // u <= 16 ZF / L-MMSE: warp-pair solver
   if (rc <= 0) return rc;
+  if (up_for(p.u) == 32) {  // LAMA, 16 < u <= 32: register-resident recursion kernel
+    rc = launch_lama(p, st);
+    if (rc <= 0) return rc;
+  }
   return launch_stats_up(up_for(p.u), p, st);
 }
 
