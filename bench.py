@@ -282,8 +282,9 @@ def kernel_name(kernel_id, wl, two_pass):
     up = 8 if wl["U"] <= 8 else 16 if wl["U"] <= 16 else 32 if wl["U"] <= 32 else 64
     tag = f"{wl['arch'].upper()}-{wl['kind']}"
     if two_pass and wl["kind"] == "lama":
-        return ("dbp::tc_kernel<32, stats> (3xTF32 tensor cores, fused statistics) + dbp::stats_kernel<32> "
-                "(LAMA recursions)")
+        stats = "fused statistics" if wl["arch"] == "pd" else "per-cluster statistics"
+        return (f"dbp::tc_kernel<32, stats> (3xTF32 tensor cores, {stats}) + dbp::lama_kernel "
+                "(LAMA recursions, G in registers" + (", cluster fusion)" if wl["arch"] == "fd" else ")"))
     if two_pass and wl["arch"] == "fd":
         return ("dbp::tcw_stats_kernel (per-cluster split-bf16 statistics) + dbp::stats_kernel<64> (cluster "
                 "solves + fusion), per item chunk")
@@ -417,7 +418,7 @@ def single_gpu(args, wl, name):
     # U = 64: statistics + solve launches (FD: per item chunk of ~3 GiB of
     # per-cluster records, whole N0 runs of W items -- dispatch fd_wide)
     two_pass = (kernel_id in (2, 3) and wl["U"] == 64 and (wl["arch"] == "pd" or kernel_id == 3)) or \
-        (kernel_id == 2 and wl["U"] == 32 and wl["kind"] == "lama" and wl["arch"] == "pd")  # stats + LAMA
+        (kernel_id == 2 and wl["U"] == 32 and wl["kind"] == "lama")  # statistics + lama_kernel
     per_step = 1
     if two_pass:
         per_step = 2

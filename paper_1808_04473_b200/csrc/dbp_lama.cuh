@@ -13,34 +13,35 @@
 // (measured: a broadcast LDS.128 costs 4 wavefronts), so an FMA-bound matvec
 // needs >= 4 FMA per word a lane reads.  Here:
 //
-//   team = 64 threads (2 warps) per unit; thread (ip, jq), ip = 8 warp +
-//   lane / 4 in [0, 16), jq = lane % 4, holds G rows ip and ip + 16, columns
-//   8 jq .. 8 jq + 7, in REGISTERS (32) for the whole recursion.  Symbols run
-//   in batches of four: every s pair a thread reads (one float4, broadcast
-//   over the rows) feeds 16 FFMA (2 rows x 2 columns), 4 FMA per word; a
-//   4-lane reduce-scatter (12 shuffles) then leaves thread jq with (G s) of
-//   symbol 4b + jq for both rows.  The owned states (y_mrc, s, v of
-//   (4b + jq, ip / ip + 16)) sit in per-thread shared-memory slots and the
-//   batch loop is not unrolled (the unrolled recursion, 34 KB of code per
-//   iteration, stalled on instruction fetch).
+//   one WARP per unit (4 independent units per CTA, no CTA barrier); lane
+//   (ip, jq), ip = lane / 2, jq = lane % 2, holds G rows ip and ip + 16,
+//   columns 16 jq .. 16 jq + 15, in REGISTERS (64) as (re, im) pairs for the
+//   whole recursion.  Symbols run in pairs: every s pair a lane reads (one
+//   float4, broadcast over the 16 lanes of a parity) feeds 8 FFMA2 -- packed
+//   FP32 on the G pair with s_r / s_i as the scalar broadcast operand, 16 FMA
+//   per 4 words -- and one shuffle exchange leaves lane jq with (G s) of
+//   symbol 2b + jq for both rows.  The owned states (y_mrc, v of
+//   (2b + jq, ip / ip + 16)) sit in per-lane shared-memory slots, s in the
+//   matvec operand array itself, and the batch loop is not unrolled (the
+//   unrolled recursion, 34 KB of code per iteration, stalled on instruction
+//   fetch).
 //
-// Per iteration: matvec, z = y_mrc + s + v - G s (lama_scale applied as in
-// the reference's rescaled statistics), the PAM-factorised posterior with the
-// two dimensions in packed FP32 pairs, the per-symbol sum of g (shuffles over
-// the warp's rows, one partial per warp), and s^{t+1} published to the other
-// half of a double-buffered shared array -- ONE CTA barrier per iteration:
-// v^{t+1} = beta phi^{t+1} / tau^t (z - s) is stored without its phi factor
-// and completed when the next pass reads phi^{t+1}.
+// Per pass over a symbol pair: matvec, z = y_mrc + s + v - G s (lama_scale
+// applied as in the reference's rescaled statistics), the PAM-factorised
+// posterior with the two dimensions in packed FP32 pairs, phi^{t+1} as a
+// shuffle reduction over the 16 lanes of the symbol (the warp holds all u
+// rows), v^{t+1} and s^{t+1} written back -- __syncwarp only.
 #pragma once
 #include "dbp_epilogue.cuh"
 
 namespace dbp {
 
-constexpr int LAMA_NT = 64;
-// shared s row: 32 columns in four octets, each octet padded by two entries
-// so the four jq lanes of a quad read four disjoint bank groups
-constexpr int LAMA_SLD = 40;
-__device__ __forceinline__ int lama_sidx(int j) { return j + 2 * (j >> 3); }
+constexpr int LAMA_WARPS = 4;  // independent units (one per warp) per CTA
+constexpr int LAMA_NT = 32 * LAMA_WARPS;
+// shared s row: 32 columns in two halves, the second shifted by two entries
+// so the two lane parities read disjoint bank groups
+constexpr int LAMA_SLD = 36;
+__device__ __forceinline__ int lama_sidx(int j) { return j + 2 * (j >> 4); }
 
 // packed FP32 pairs (one 64-bit register pair; FFMA2 / FADD2 / FMUL2 on sm_100)
 typedef unsigned long long p2_t;
@@ -123,51 +124,50 @@ __device__ __forceinline__ void lama_post2(float2 z, float tinv, const ConstPara
 }
 
 #ifndef DBP_LAMA_MINB
-#define DBP_LAMA_MINB 8  // CTAs per SM the register budget is cut for (study builds vary it)
+#define DBP_LAMA_MINB 3  // CTAs per SM (the shared-memory limit) the register budget is cut for (study builds vary it)
 #endif
+// per-warp shared-memory block (one unit / item per warp)
+struct __align__(16) LamaWarpSmem {
+  float2 S[MAX_T][LAMA_SLD];      // s per (symbol, column): the matvec operand
+  float2 ZY[MAX_T / 2][2][32];    // per-lane state slots: y_mrc (z^{t_max} at the end),
+  float2 VV[MAX_T / 2][2][32];    // v,
+  float2 FN[MAX_T / 2][2][32];    // FD: fusion numerators sum_c w_c z_c
+  float FD[MAX_T / 2][32];        // FD: fusion denominators sum_c w_c
+  float PH[MAX_T / 2][2];         // phi per symbol (batch b, lane parity)
+  float wb[MAX_C][MAX_T];         // FD: cluster weights (for nu)
+  int flags[2];
+};
+
 template <int PL>
 __global__ void __launch_bounds__(LAMA_NT, DBP_LAMA_MINB) lama_kernel(const __grid_constant__ EqParams p) {
-  __shared__ __align__(16) float2 S[2][MAX_T][LAMA_SLD];  // s per (symbol, column), double-buffered
-  __shared__ __align__(16) float2 P[2][MAX_T];            // per-warp sums of g per symbol
-  __shared__ float2 ZY[4][2][LAMA_NT];                    // per-thread state slots: y_mrc (z at the end),
-  __shared__ float2 SS[4][2][LAMA_NT];                    // s,
-  __shared__ float2 VV[4][2][LAMA_NT];                    // v / phi' (equalize.py:252)
-  __shared__ float2 fnum[4][2][LAMA_NT];                  // FD: per-thread fusion sums
-  __shared__ float fden[4][LAMA_NT];
-  __shared__ float wb[MAX_C][MAX_T];                      // FD: cluster weights (for nu)
-  __shared__ int flags[2];
+  extern __shared__ __align__(16) char lama_smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ip = warp * 8 + (lane >> 2), jq = lane & 3;
-  const int u = p.u, T = p.T;
+  LamaWarpSmem& ws = reinterpret_cast<LamaWarpSmem*>(lama_smem)[warp];
+  const int ip = lane >> 1, jq = lane & 1;  // rows ip, ip + 16; columns 16 jq .. 16 jq + 15
+  const int u = p.u, T = p.T, nb = (T + 1) >> 1;
   const bool fd = p.arch == ARCH_FD;
   const bool herm = p.g_hermitian != 0;
   const int ncl = fd ? p.C : 1;
   const size_t rec = (size_t)u * u + (size_t)T * u;
   const int64_t nrec = p.n_items * ncl;
+  const int64_t nwarps = (int64_t)gridDim.x * LAMA_WARPS;
   const float inv_u = 1.f / (float)u;
   const float damp = p.damping;
   const ConstParams& cp = p.cp;
 
   // padding rows / columns of s stay zero for the whole launch
-  for (int e = tid; e < 2 * MAX_T * LAMA_SLD; e += LAMA_NT) (&S[0][0][0])[e] = make_float2(0.f, 0.f);
-  bool valid[4][2];
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int r = 0; r < 2; ++r) valid[b][r] = 4 * b + jq < T && ip + 16 * r < u;
+  for (int e = lane; e < MAX_T * LAMA_SLD; e += 32) (&ws.S[0][0])[e] = make_float2(0.f, 0.f);
+  __syncwarp();
 
-  for (int64_t n = blockIdx.x; n < p.n_items; n += gridDim.x) {
-    if (tid == 0) {
-      flags[0] = 0;
-      flags[1] = 0x7fffffff;
-    }
+  for (int64_t n = (int64_t)blockIdx.x * LAMA_WARPS + warp; n < p.n_items; n += nwarps) {
     const float n0i = item_n0(p, n);
+    int dv = 0x7fffffff, st = 0;  // first divergent iteration; status of the item
     for (int c = 0; c < ncl; ++c) {
       const int64_t rr = n * ncl + c;
       const float2* src = p.stats_in + rr * rec;
-      {  // the next record into L2 while this one iterates
-        const int64_t rn = (c + 1 < ncl) ? rr + 1 : (n + gridDim.x) * ncl;
-        if (tid == 0 && rn < nrec) {
+      {  // the warp's next record into L2 while this one iterates
+        const int64_t rn = (c + 1 < ncl) ? rr + 1 : (n + nwarps) * ncl;
+        if (lane == 0 && rn < nrec) {
           const char* nx = reinterpret_cast<const char*>(p.stats_in + rn * rec);
           const uint32_t bytes = (uint32_t)(rec * sizeof(float2));
           for (uint32_t o = 0; o < bytes; o += 32768) {
@@ -177,190 +177,191 @@ __global__ void __launch_bounds__(LAMA_NT, DBP_LAMA_MINB) lama_kernel(const __gr
           }
         }
       }
-      // G rows ip and ip + 16, columns 8 jq .. 8 jq + 7 (the kernel's own
-      // Gram: conj of the columns, as the streaming kernels read it)
-      float2 g[2][8];
+      // G rows ip and ip + 16, columns 16 jq .. 16 jq + 15, in registers as
+      // natural (re, im) pairs; the kernel's own Gram (herm) is read down the
+      // columns, G[j][i] = conj G[i][j], the conjugation folded into the
+      // recombination below
+      p2_t g[2][16];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int i = ip + 16 * r;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = 8 * jq + k;
-          float2 x = make_float2(0.f, 0.f);
-          if (i < u && j < u) x = herm ? c_conj(src[(size_t)j * u + i]) : src[(size_t)i * u + j];
-          g[r][k] = x;
+        for (int k = 0; k < 16; ++k) {
+          const int j = 16 * jq + k;
+          g[r][k] = (i < u && j < u) ? *reinterpret_cast<const p2_t*>(src + (herm ? (size_t)j * u + i : (size_t)i * u + j))
+                                     : 0ull;
         }
       }
+      const float hs = herm ? -1.f : 1.f;
       const float sc = fd ? p.cl_scale[c] : p.lama_scale;
       const float beta = fd ? p.cl_beta[c] : p.beta;
       const float n0 = n0i * sc;
-      __syncthreads();  // the previous unit's last matvec has read S
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int t = 4 * b + jq;
+      __syncwarp();  // the previous unit's reads of S / ZY are done
+      for (int b = 0; b < nb; ++b) {
+        const int t = 2 * b + jq;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int i = ip + 16 * r;
-          const float2 s0 = valid[b][r] ? cp.mean : make_float2(0.f, 0.f);
-          ZY[b][r][tid] = valid[b][r] ? c_scale(src[(size_t)u * u + (size_t)t * u + i], sc) : make_float2(0.f, 0.f);
-          SS[b][r][tid] = s0;
-          VV[b][r][tid] = make_float2(0.f, 0.f);
-          if (valid[b][r]) S[0][t][lama_sidx(i)] = s0;
+          const bool ok = t < T && i < u;
+          ws.ZY[b][r][lane] = ok ? c_scale(src[(size_t)u * u + (size_t)t * u + i], sc) : make_float2(0.f, 0.f);
+          ws.VV[b][r][lane] = make_float2(0.f, 0.f);
+          if (ok) ws.S[t][lama_sidx(i)] = cp.mean;
         }
+        if (ip == 0) ws.PH[b][jq] = cp.es;
       }
-      __syncthreads();
-      int par = 0, dv = 0x7fffffff;  // dv: first divergent iteration of this thread's states
       for (int it = 1;; ++it) {
         const bool last = it == p.t_max;
-        // one batch of four symbols per pass (a compact loop body: the fully
-        // unrolled recursion missed the instruction cache); the owned states
-        // (z, s, v of rows ip, ip + 16) live in per-thread shared-memory slots
 #pragma unroll 1
-        for (int b = 0; b < 4; ++b) {
-          const int t = 4 * b + jq;
-          // phi^t: the per-symbol mean of g from the previous pass (equalize.py:253)
-          const float2 pw = P[par ^ 1][t];
-          const float phi = it == 1 ? cp.es : (pw.x + pw.y) * inv_u;
-          // ---- (G s)_i for rows ip, ip + 16 and symbols 4b..4b+3 over this
-          // thread's eight columns: each s pair read from shared memory feeds
-          // 16 FFMA (two rows); rows t >= T of S are zero
-          float2 a[2][4];
+        for (int b = 0; b < nb; ++b) {
+          __syncwarp();  // S rows 2b, 2b + 1 of the previous pass are published
+          const int t = 2 * b + jq;
+          // ---- (G s)_i for rows ip, ip + 16 and symbols 2b, 2b + 1 over this
+          // lane's 16 columns: FFMA2 on (re, im) pairs of G with s_r / s_i as
+          // the broadcast scalar operand, A += g s_r, B += g s_i; each s pair
+          // read (one float4, shared by the 16 lanes of a parity) feeds 8 FFMA2
+          // = 16 FMA; rows t >= T of S are zero
+          p2_t pa[2][2], pb[2][2];  // [row][symbol]
 #pragma unroll
-          for (int r = 0; r < 2; ++r)
+          for (int r = 0; r < 2; ++r) pa[r][0] = pa[r][1] = pb[r][0] = pb[r][1] = 0ull;
+          const float2* sb = &ws.S[2 * b][lama_sidx(16 * jq)];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a[r][q] = make_float2(0.f, 0.f);
-          const float2* sb = &S[par][4 * b][10 * jq];  // lama_sidx(8 jq) = 10 jq
+          for (int k2 = 0; k2 < 8; ++k2) {
 #pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 2; ++q) {
               const float4 sv = *reinterpret_cast<const float4*>(sb + q * LAMA_SLD + 2 * k2);
-              const float2 s0 = make_float2(sv.x, sv.y), s1 = make_float2(sv.z, sv.w);
 #pragma unroll
               for (int r = 0; r < 2; ++r) {
-                c_fma(a[r][q], g[r][2 * k2], s0);
-                c_fma(a[r][q], g[r][2 * k2 + 1], s1);
+                pa[r][q] = p2_fma(g[r][2 * k2], p2(sv.x, sv.x), pa[r][q]);
+                pb[r][q] = p2_fma(g[r][2 * k2], p2(sv.y, sv.y), pb[r][q]);
+                pa[r][q] = p2_fma(g[r][2 * k2 + 1], p2(sv.z, sv.z), pa[r][q]);
+                pb[r][q] = p2_fma(g[r][2 * k2 + 1], p2(sv.w, sv.w), pb[r][q]);
               }
             }
           }
-          // reduce-scatter over the quad: lane jq keeps symbol 4b + jq
-          const bool h1 = (jq & 2) != 0, h0 = (jq & 1) != 0;
+          // (G s) = (A.re - B.im, B.re + A.im); conj(G) s = (A.re + B.im, B.re - A.im)
+          float2 a[2][2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const float2 A = p2_unpack(pa[r][q]), B = p2_unpack(pb[r][q]);
+              a[r][q] = make_float2(fmaf(-hs, B.y, A.x), fmaf(hs, A.y, B.x));
+            }
+          // the lane pair exchanges halves: lane jq keeps symbol 2b + jq
           float2 m[2];
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
-            float2 k0 = h1 ? a[r][2] : a[r][0], k1 = h1 ? a[r][3] : a[r][1];
-            const float2 o0 = h1 ? a[r][0] : a[r][2], o1 = h1 ? a[r][1] : a[r][3];
-            k0.x += __shfl_xor_sync(0xffffffffu, o0.x, 2);
-            k0.y += __shfl_xor_sync(0xffffffffu, o0.y, 2);
-            k1.x += __shfl_xor_sync(0xffffffffu, o1.x, 2);
-            k1.y += __shfl_xor_sync(0xffffffffu, o1.y, 2);
-            m[r] = h0 ? k1 : k0;
-            const float2 om = h0 ? k0 : k1;
-            m[r].x += __shfl_xor_sync(0xffffffffu, om.x, 1);
-            m[r].y += __shfl_xor_sync(0xffffffffu, om.y, 1);
+            m[r] = jq ? a[r][1] : a[r][0];
+            const float2 o = jq ? a[r][0] : a[r][1];
+            m[r].x += __shfl_xor_sync(0xffffffffu, o.x, 1);
+            m[r].y += __shfl_xor_sync(0xffffffffu, o.y, 1);
           }
+          const float phi = ws.PH[b][jq];
           const float tau = n0 + beta * phi;
           const float tinv = rcp_ftz(fmaxf(tau, FLT_MIN));  // MUFU.RCP (~1 ulp)
+          float2 z[2], sold[2], F[2];
           float gs = 0.f;
+          __syncwarp();  // every lane has read S rows 2b, 2b + 1
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             const int i = ip + 16 * r;
-            const bool ok = 4 * b + jq < T && i < u;
-            const float2 sold = SS[b][r][tid];
-            // v^t = beta phi^t / tau^{t-1} (z^{t-1} - s^{t-1}): the stored part times phi^t
-            const float2 v = it == 1 ? make_float2(0.f, 0.f) : c_scale(VV[b][r][tid], phi);
+            const bool ok = t < T && i < u;
+            sold[r] = ws.S[t][lama_sidx(i)];
             // z = y_mrc + (I - G) s + v (equalize.py:243); |z|^2 < 1e36 is
             // false for NaN / inf too (equalize.py:246-249)
-            const float2 z = c_sub(c_add(ZY[b][r][tid], c_add(sold, v)), c_scale(m[r], sc));
-            dv = (ok && !(c_abs2(z) < DIVERGE_ABS2)) ? min(dv, it) : dv;
-            if (last) {  // z^{t_max} parked in the (now unused) y_mrc slot
-              ZY[b][r][tid] = z;
+            z[r] = c_sub(c_add(ws.ZY[b][r][lane], c_add(sold[r], ws.VV[b][r][lane])), c_scale(m[r], sc));
+            dv = (ok && !(c_abs2(z[r]) < DIVERGE_ABS2)) ? min(dv, it) : dv;
+            if (last) {
+              ws.ZY[b][r][lane] = z[r];  // z^{t_max} parked in the y_mrc slot
               continue;
             }
-            // ---- denoiser; s^{t+1} published
-            float2 F;
             float gv;
             if constexpr (PL > 0)
-              lama_post2<PL>(z, tinv, cp, F, gv);
+              lama_post2<PL>(z[r], tinv, cp, F[r], gv);
             else
-              posterior_t<0>(z, tau, cp, F, gv);
+              posterior_t<0>(z[r], tau, cp, F[r], gv);
             gs += ok ? gv : 0.f;
-            VV[b][r][tid] = c_scale(c_sub(z, sold), beta * tinv);
-            const float2 snew = c_add(c_scale(F, damp), c_scale(sold, 1.f - damp));
-            SS[b][r][tid] = snew;
-            if (ok) S[par ^ 1][t][lama_sidx(i)] = snew;
           }
-          if (!last) {  // this batch's sums of g over the warp's rows -> P
+          if (last) continue;
+          // phi^{t+1}: mean of g over the u rows of symbol t (equalize.py:253),
+          // the 16 lanes of this parity hold them all
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
-            if (lane < 4) (warp ? P[par][t].y : P[par][t].x) = gs;
+          for (int o = 2; o < 32; o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+          const float phin = gs * inv_u;
+          const float coef = beta * phin * tinv;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int i = ip + 16 * r;
+            ws.VV[b][r][lane] = c_scale(c_sub(z[r], sold[r]), coef);
+            const float2 snew = c_add(c_scale(F[r], damp), c_scale(sold[r], 1.f - damp));
+            if (t < T && i < u) ws.S[t][lama_sidx(i)] = snew;
           }
+          __syncwarp();  // every lane has read PH[b] before it is overwritten
+          if (ip == 0) ws.PH[b][jq] = phin;
         }
         if (last) break;
-        __syncthreads();
-        par ^= 1;
       }
-      if (dv < 0x7fffffff) atomicMin(&flags[1], dv);
       // ---- outputs (equalize.py:255-257): z^{t_max}, tau^{t_max}
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int t = 4 * b + jq;
-        const float2 pw = P[par ^ 1][t];
-        const float phi = p.t_max == 1 ? cp.es : (pw.x + pw.y) * inv_u;
-        const float tau = n0 + beta * phi;
+      __syncwarp();
+      for (int b = 0; b < nb; ++b) {
+        const int t = 2 * b + jq;
+        const float tau = n0 + beta * ws.PH[b][jq];
         const float wt = 1.f / fmaxf(tau, VAR_FLOOR);  // FD: w = 1 / max(tau, 1e-15) (fusion.py:96-105)
-        if (fd && t < T && ip < u && !(tau > 0.f)) set_status(flags, ST_BADVAR);
+        if (fd && t < T && ip < u && !(tau > 0.f)) st = ST_BADVAR;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int i = ip + 16 * r;
-          const float2 z = ZY[b][r][tid];
+          const float2 z = ws.ZY[b][r][lane];
           if (!fd) {
-            if (valid[b][r]) {
+            if (t < T && i < u) {
               const size_t o = ((size_t)n * T + t) * u + i;
               p.xhat[o] = z;
               if (p.dec) p.dec[o] = (uint8_t)slice_symbol(z, cp);
             }
           } else {  // fold cluster c
             const float2 x = c_scale(z, wt);
-            fnum[b][r][tid] = c == 0 ? x : c_add(fnum[b][r][tid], x);
+            ws.FN[b][r][lane] = c == 0 ? x : c_add(ws.FN[b][r][lane], x);
           }
         }
         if (fd) {
-          fden[b][tid] = c == 0 ? wt : fden[b][tid] + wt;
-          if (ip == 0 && t < T) wb[c][t] = wt;
+          ws.FD[b][lane] = c == 0 ? wt : ws.FD[b][lane] + wt;
+          if (ip == 0 && t < T) ws.wb[c][t] = wt;
         } else if (ip == 0 && t < T) {
           p.sigma2[(size_t)n * T + t] = tau;
         }
       }
     }
     if (fd) {  // fuse_estimates (fusion.py:108-124); sigma2 = 1 / sum_c 1 / tau_c
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int t = 4 * b + jq;
-        const float den = fden[b][tid];
+      for (int b = 0; b < nb; ++b) {
+        const int t = 2 * b + jq;
+        const float den = ws.FD[b][lane];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int i = ip + 16 * r;
-          if (valid[b][r]) {
-            const float2 x = c_scale(fnum[b][r][tid], 1.f / den);
+          if (t < T && i < u) {
+            const float2 x = c_scale(ws.FN[b][r][lane], 1.f / den);
             const size_t o = ((size_t)n * T + t) * u + i;
             p.xhat[o] = x;
             if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, cp);
           }
-          if (i == 0 && t < T) {
-            p.sigma2[(size_t)n * T + t] = 1.f / den;
-            if (p.nu)
-              for (int cc = 0; cc < ncl; ++cc) p.nu[((size_t)n * ncl + cc) * T + t] = wb[cc][t] / den;
-          }
+        }
+        if (ip == 0 && t < T) {
+          p.sigma2[(size_t)n * T + t] = 1.f / den;
+          if (p.nu)
+            for (int cc = 0; cc < ncl; ++cc) p.nu[((size_t)n * ncl + cc) * T + t] = ws.wb[cc][t] / den;
         }
       }
     }
-    __syncthreads();  // every status / divergence update of the item is in
-    if (tid == 0) {
-      int st = flags[0];
-      if (flags[1] < 0x7fffffff) st = st ? st : ST_DIVERGED;
+    // item status: BadVariance first (set during the folds), else divergence
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dv = min(dv, __shfl_xor_sync(0xffffffffu, dv, o));
+      st = max(st, __shfl_xor_sync(0xffffffffu, st, o));
+    }
+    if (lane == 0) {
+      if (dv < 0x7fffffff) st = st ? st : ST_DIVERGED;
       p.status[n] = st;
-      if (p.iters) p.iters[n] = (flags[1] < 0x7fffffff) ? flags[1] : 0;
+      if (p.iters) p.iters[n] = (dv < 0x7fffffff) ? dv : 0;
     }
   }
 }

@@ -25,7 +25,8 @@ cap() {  # name config kernel-regex skip
 }
 cap cfg2 cfg2 tc2_kernel 4
 cap cfg3zf cfg3-zf tc2_kernel 4
-cap cfg4fd cfg4-fd stream_kernel 3
+cap cfg4fd cfg4-fd lama_kernel 2
+cap cfg4pd cfg4-pd lama_kernel 2
 cap cfg5pd512_stats cfg5-pd512 tcw_stats 3
 cap cfg5pd512_solve cfg5-pd512 ^stats_kernel 3
 cap cfg1 cfg1 tc2_kernel 4
