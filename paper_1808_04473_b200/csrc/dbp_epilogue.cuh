@@ -419,8 +419,8 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          c_fms(m[r][c], cr[r][0], rr[0][c]);
-          c_fms(m[r][c], cr[r][1], rr[1][c]);
+          c_fms2(m[r][c], cr[r][0], rr[0][c]);
+          c_fms2(m[r][c], cr[r][1], rr[1][c]);
         }
     }
     __syncwarp();  // the warp's Ct / C / Pinv reads are done before the next block rewrites them
@@ -602,11 +602,11 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
       const float4 av = *reinterpret_cast<const float4*>(arow + jj);
       const float4 b0 = *reinterpret_cast<const float4*>(z0 + jj);
       const float4 b1 = *reinterpret_cast<const float4*>(z1 + jj);
-      c_fma(acc0, make_float2(av.x, av.y), make_float2(b0.x, b0.y));
-      c_fma(acc1, make_float2(av.x, av.y), make_float2(b1.x, b1.y));
+      c_fma2(acc0, make_float2(av.x, av.y), make_float2(b0.x, b0.y));
+      c_fma2(acc1, make_float2(av.x, av.y), make_float2(b1.x, b1.y));
       if (jj + 1 < u) {
-        c_fma(acc0, make_float2(av.z, av.w), make_float2(b0.z, b0.w));
-        c_fma(acc1, make_float2(av.z, av.w), make_float2(b1.z, b1.w));
+        c_fma2(acc0, make_float2(av.z, av.w), make_float2(b0.z, b0.w));
+        c_fma2(acc1, make_float2(av.z, av.w), make_float2(b1.z, b1.w));
       }
     }
     if (unb) {
