@@ -382,7 +382,7 @@ __device__ __forceinline__ void t2_gj2d(float2* Gw, int LD, int u, float rho, bo
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) c_fms(m[r][c], cr[r], rr[c]);
+        for (int c = 0; c < 4; ++c) c_fms2(m[r][c], cr[r], rr[c]);
     }
   }
 #pragma unroll
@@ -406,7 +406,10 @@ __device__ __forceinline__ void t2_gj2d(float2* Gw, int LD, int u, float rho, bo
 // zpotrf's "not positive definite").  PD writes x-hat / decisions / sigma2 /
 // gain / status; FD adds w z, w, 1/sigma2 (w = 1/max(sigma2, 1e-15), MRC: the
 // Gram diagonal, fusion.py:96-105,149-151) to the half-warp's sums in `acc`.
-template <bool FD>
+// F2: FFMA2 complex MACs in the A y products (measured: cfg2 -2 %, cfg3-zf
+// -1.5 %; off in the FD two-part instantiation, which only MRC runs and whose
+// MRC path measured 5 % slower with the FFMA2 variant compiled in)
+template <bool FD, bool F2 = true>
 __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n, const int* c, const float* n0,
                               const bool* valid, int lane, const T2FdAcc* acc = nullptr) {
   const int h = lane >> 4, j = lane & 15;
@@ -484,10 +487,17 @@ __device__ void t2_solve_pair(const Work* w, const EqParams& p, const int64_t* n
           for (int e = 0; e < 4; ++e) {
             const int i = i0 + 2 * e;
             // y_t[i] beyond u is zero (the recombination zeroes it; its A column is zero)
-            c_fma_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
-            c_fma_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
-            c_fma_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
-            c_fma_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+            if constexpr (F2) {
+              c_fma2_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
+              c_fma2_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
+              c_fma2_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
+              c_fma2_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+            } else {
+              c_fma_conj(a0, m[i], make_float2(y0[e].x, y0[e].y));
+              c_fma_conj(b0, m[i], make_float2(y1[e].x, y1[e].y));
+              c_fma_conj(a1, m[i + 1], make_float2(y0[e].z, y0[e].w));
+              c_fma_conj(b1, m[i + 1], make_float2(y1[e].z, y1[e].w));
+            }
           }
         }
       }
@@ -594,7 +604,7 @@ __device__ void t2_solve_quad(const Work* w, const EqParams& p, const int64_t* n
       const float2 r = (j == k) ? make_float2(1.f + rp, 0.f) : c_scale(m[k], rp);
       cc[k] = make_float2(pv - 1.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) c_fms(m[i], cc[i], r);
+      for (int i = 0; i < 8; ++i) c_fms2(m[i], cc[i], r);
     }
   }
   float ajj = 0.f, off = 0.f;
@@ -640,8 +650,8 @@ __device__ void t2_solve_quad(const Work* w, const EqParams& p, const int64_t* n
         for (int i = 0; i < 8; i += 2) {
           if (i >= u) break;
           const float4 y = *reinterpret_cast<const float4*>(z + i);  // y_t[i] beyond u is zero
-          c_fma_conj(a0, m[i], make_float2(y.x, y.y));
-          c_fma_conj(a1, m[i + 1], make_float2(y.z, y.w));
+          c_fma2_conj(a0, m[i], make_float2(y.x, y.y));
+          c_fma2_conj(a1, m[i + 1], make_float2(y.z, y.w));
         }
       }
     }
@@ -1183,7 +1193,7 @@ __global__ void __maxnreg__(16384 / (32 * ((T2_THREADS / 32 + 3) / 4)) / 8 * 8)
           if (lane == 0) *acc.st = 0;
           __syncwarp();
         }
-        t2_solve_pair<true>(w, p, n, c, n0, valid, lane, &acc);
+        t2_solve_pair<true, NSPLIT != 2>(w, p, n, c, n0, valid, lane, &acc);
         __syncwarp();
         const int clast = (lbk[1] >= 0) ? c[1] : c[0];
         if (item_ok && clast == upi - 1) t2_fd_finish(acc, p, n[0], lane);
