@@ -283,7 +283,9 @@ def kernel_name(kernel_id, wl, two_pass):
     tag = f"{wl['arch'].upper()}-{wl['kind']}"
     if two_pass and wl["kind"] == "lama":
         stats = "fused statistics" if wl["arch"] == "pd" else "per-cluster statistics"
-        return (f"dbp::tc_kernel<32, stats> (3xTF32 tensor cores, {stats}) + dbp::lama_kernel "
+        skern = ("dbp::tcw_stats_kernel<3> (split-bf16 tensor cores" if kernel_id == 3
+                 else "dbp::tc_kernel<32, stats> (3xTF32 tensor cores")
+        return (f"{skern}, {stats}) + dbp::lama_kernel "
                 "(LAMA recursions, G in registers" + (", cluster fusion)" if wl["arch"] == "fd" else ")"))
     if two_pass and wl["arch"] == "fd":
         return ("dbp::tcw_stats_kernel (per-cluster split-bf16 statistics) + dbp::stats_kernel<64> (cluster "
@@ -418,7 +420,7 @@ def single_gpu(args, wl, name):
     # U = 64: statistics + solve launches (FD: per item chunk of ~3 GiB of
     # per-cluster records, whole N0 runs of W items -- dispatch fd_wide)
     two_pass = (kernel_id in (2, 3) and wl["U"] == 64 and (wl["arch"] == "pd" or kernel_id == 3)) or \
-        (kernel_id == 2 and wl["U"] == 32 and wl["kind"] == "lama")  # statistics + lama_kernel
+        (kernel_id in (2, 3) and wl["U"] == 32 and wl["kind"] == "lama")  # statistics + lama_kernel
     per_step = 1
     if two_pass:
         per_step = 2

@@ -79,8 +79,8 @@ const char* dbp_last_error(void);
  * launched (DBP_KERNEL_*; 0 = none).  Introspection only (tests and
  * benchmarks); no reference counterpart. */
 #define DBP_KERNEL_AUTO 0
-#define DBP_KERNEL_SIMT 1     /* FP32-SIMT streaming kernel (U = 64, ragged clusters, LAMA) */
-#define DBP_KERNEL_TC_TF32 2  /* 3xTF32 tensor-core streaming kernel (U <= 32; U = 64 statistics) */
+#define DBP_KERNEL_SIMT 1     /* FP32-SIMT streaming kernel (ragged clusters, LAMA at u <= 16) */
+#define DBP_KERNEL_TC_TF32 2  /* 3xTF32 tensor-core kernel (U <= 32; LAMA 16 < u <= 32: statistics + lama_kernel) */
 #define DBP_KERNEL_TC_BF16 3  /* split-bf16 tensor-core streaming kernel (U <= 16 linear / statistics) */
 int dbp_last_kernel(void);
 

@@ -558,7 +558,11 @@ static int fd_wide(EqParams& p, cudaStream_t st, int up = 64) {
     s.arch = ARCH_STATS;
     s.sum_clusters = 0;
     s.stats_out = stats;
+    // up = 32 (FD LAMA): the 3xTF32 kernel -- per-cluster units of 32 antennas
+    // are one stage each, where the wide split-bf16 kernel measured slower
+    // (cfg4-fd 8.85 -> 10.76 ms)
     int rc = up == 64 ? launch_tcw(s, st, 3) : launch_tc_up(up, s, st);
+    g_last_kernel = up == 64 ? DBP_KERNEL_TC_BF16 : DBP_KERNEL_TC_TF32;
     if (rc) return rc;  // 1: geometry not covered (the same for every chunk)
     q.stats_in = stats;
     rc = launch_lama(q, st);  // LAMA (u <= 32): the register-resident recursion kernel
@@ -606,10 +610,19 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
     const size_t rec = (size_t)p.u * p.u + (size_t)p.T * p.u;
     q.stats_out = static_cast<float2*>(stream_scratch(st, (size_t)p.n_items * rec * sizeof(float2)));
     if (!q.stats_out) return fail(DBP_E_CUDA, "statistics scratch allocation failed");
-    int rc = launch_tc_up(32, q, st);
+    // split-bf16 statistics (wide kernel, half of M = 128 used), three parts:
+    // cfg4-pd 1.99 -> 1.66 ms against the 3xTF32 kernel (two parts: 1.54 ms,
+    // but x-hat 7.7e-6 and decision flips at 8.7e-6 of the symbols, too close
+    // to the 1e-5 bar)
+    int kid = DBP_KERNEL_TC_BF16;
+    int rc = pol != DBP_KERNEL_TC_TF32 ? launch_tcw(q, st, 3) : 1;
+    if (rc == 1) {
+      kid = DBP_KERNEL_TC_TF32;
+      rc = launch_tc_up(32, q, st);
+    }
     if (rc < 0) return rc;
     if (rc == 0) {
-      g_last_kernel = DBP_KERNEL_TC_TF32;
+      g_last_kernel = kid;
       EqParams r = p;
       r.stats_in = q.stats_out;
       r.C = 1;
@@ -622,8 +635,7 @@ static int dispatch_stream(EqParams& p, cudaStream_t st) {
   // the recursions and their fusion in lama_kernel (G in registers)
   if (!force_simt && up == 32 && p.arch == ARCH_FD && p.kind == EQ_LAMA && !opt(DBP_OPT_NO_WIDE) && !p.tr_z &&
       opt(DBP_OPT_LAMA_KERNEL) != 1) {
-    const int rc = fd_wide(p, st, 32);
-    if (rc == 0) g_last_kernel = DBP_KERNEL_TC_TF32;
+    const int rc = fd_wide(p, st, 32);  // sets g_last_kernel (the statistics kernel)
     if (rc <= 0) return rc;
   }
   if (!force_simt && up == 64 && p.arch == ARCH_FD && p.kind != EQ_LAMA && !opt(DBP_OPT_NO_WIDE) &&

@@ -183,7 +183,9 @@ int launch_t2_stats_solve(EqParams& p, cudaStream_t st) {
 // (summed over the clusters, or per uniform cluster); K a multiple of 32.
 // Returns 1 when the geometry is not covered (caller falls back).
 int launch_tcw(EqParams& p, cudaStream_t st, int nsplit_default) {
-  if (p.arch != ARCH_STATS || p.u <= 32 || p.u > 64 || p.us > 64 || p.T > 16) return 1;
+  // 16 < u <= 32 fills half of the M = 128 rows (the PD LAMA statistics: two
+  // bf16 parts on the tensor cores beat the 3xTF32 kernel's four tf32 products)
+  if (p.arch != ARCH_STATS || p.u <= 16 || p.u > 64 || p.us > 64 || p.T > 16) return 1;
   const int upi = p.sum_clusters ? 1 : p.C;
   if (p.B % upi) return 1;
   const int K = p.B / upi;
