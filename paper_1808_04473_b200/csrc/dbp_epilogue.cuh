@@ -340,7 +340,7 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
         bad = true;
         p = 1.f;
       }
-      const float rp = __frcp_rn(p);
+      const float rp = rcp_pivot(p);
       const float2 rj = (pc == k) ? make_float2(1.f + rp, 0.f) : make_float2(rkx * rp, rky * rp);
       const float2 ci0 = (pr == k) ? make_float2(p - 1.f, 0.f) : make_float2(c0x, c0y);
       const float2 ci1 = (pr + 1 == k) ? make_float2(p - 1.f, 0.f) : make_float2(c1x, c1y);
