@@ -320,8 +320,14 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 // reduce-scatter; linear_equalize / lama_equalize API; and FD at U = 64, where
 // the records are the per-cluster statistics [n][C] of the wide tensor-core
 // kernel and each item's clusters are solved and fused in order).
+// U = 64: three CTAs per SM (80 registers, a few spills): the blocked
+// Gauss-Jordan waits on its pivot-block chain at the barriers and a third
+// item per SM fills them (cfg5-pd512 13.3 -> 12.7 ms, fd512 75.6 -> 71.6 ms)
+#ifndef DBP_STATS64_MINB
+#define DBP_STATS64_MINB 3
+#endif
 template <int UP, int NT>
-__global__ void __launch_bounds__(NT) stats_kernel(const __grid_constant__ EqParams p) {
+__global__ void __launch_bounds__(NT, (UP == 64 ? DBP_STATS64_MINB : 1)) stats_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
   const bool lama = p.kind == EQ_LAMA;
