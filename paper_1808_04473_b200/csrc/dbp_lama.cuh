@@ -124,15 +124,13 @@ __device__ __forceinline__ void lama_post2(float2 z, float tinv, const ConstPara
 }
 
 #ifndef DBP_LAMA_MINB
-#define DBP_LAMA_MINB 3  // CTAs per SM (the shared-memory limit) the register budget is cut for (study builds vary it)
+#define DBP_LAMA_MINB 4  // CTAs per SM the register budget is cut for (study builds vary it)
 #endif
 // per-warp shared-memory block (one unit / item per warp)
 struct __align__(16) LamaWarpSmem {
   float2 S[MAX_T][LAMA_SLD];      // s per (symbol, column): the matvec operand
   float2 ZY[MAX_T / 2][2][32];    // per-lane state slots: y_mrc (z^{t_max} at the end),
   float2 VV[MAX_T / 2][2][32];    // v,
-  float2 FN[MAX_T / 2][2][32];    // FD: fusion numerators sum_c w_c z_c
-  float FD[MAX_T / 2][32];        // FD: fusion denominators sum_c w_c
   float PH[MAX_T / 2][2];         // phi per symbol (batch b, lane parity)
   float wb[MAX_C][MAX_T];         // FD: cluster weights (for nu)
   int flags[2];
@@ -318,13 +316,13 @@ __global__ void __launch_bounds__(LAMA_NT, DBP_LAMA_MINB) lama_kernel(const __gr
               p.xhat[o] = z;
               if (p.dec) p.dec[o] = (uint8_t)slice_symbol(z, cp);
             }
-          } else {  // fold cluster c
+          } else if (t < T && i < u) {  // fold cluster c: sum_c w_c z_c, in x-hat itself (L2)
+            const size_t o = ((size_t)n * T + t) * u + i;
             const float2 x = c_scale(z, wt);
-            ws.FN[b][r][lane] = c == 0 ? x : c_add(ws.FN[b][r][lane], x);
+            p.xhat[o] = c == 0 ? x : c_add(p.xhat[o], x);
           }
         }
         if (fd) {
-          ws.FD[b][lane] = c == 0 ? wt : ws.FD[b][lane] + wt;
           if (ip == 0 && t < T) ws.wb[c][t] = wt;
         } else if (ip == 0 && t < T) {
           p.sigma2[(size_t)n * T + t] = tau;
@@ -332,15 +330,18 @@ __global__ void __launch_bounds__(LAMA_NT, DBP_LAMA_MINB) lama_kernel(const __gr
       }
     }
     if (fd) {  // fuse_estimates (fusion.py:108-124); sigma2 = 1 / sum_c 1 / tau_c
+      __syncwarp();  // the cluster weights wb are in
       for (int b = 0; b < nb; ++b) {
         const int t = 2 * b + jq;
-        const float den = ws.FD[b][lane];
+        float den = 0.f;  // sum_c w_c, in cluster order
+        if (t < T)
+          for (int cc = 0; cc < ncl; ++cc) den += ws.wb[cc][t];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int i = ip + 16 * r;
           if (t < T && i < u) {
-            const float2 x = c_scale(ws.FN[b][r][lane], 1.f / den);
             const size_t o = ((size_t)n * T + t) * u + i;
+            const float2 x = c_scale(p.xhat[o], 1.f / den);
             p.xhat[o] = x;
             if (p.dec) p.dec[o] = (uint8_t)slice_symbol(x, cp);
           }
