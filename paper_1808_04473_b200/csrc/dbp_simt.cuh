@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 // U = 64: three CTAs per SM (80 registers, a few spills): the blocked
 // Gauss-Jordan waits on its pivot-block chain at the barriers and a third
 // item per SM fills them (cfg5-pd512 13.3 -> 12.7 ms, fd512 75.6 -> 71.6 ms)
+#ifndef DBP_STATS_LA
+#define DBP_STATS_LA true  // U = 64 solve: look-ahead pivot-block inversion on one warp
+#endif
 #ifndef DBP_STATS64_MINB
 #define DBP_STATS64_MINB 3
 #endif
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(NT, (UP == 64 ? DBP_STATS64_MINB : 1)) stats_k
       }
       __syncthreads();
       // two CTAs per SM: look-ahead solve
-      unit_epilogue<UP, Team<NT, 0>, -1, true>(w, p, n, c, c + 1 == ncl, cl_first, tm);
+      unit_epilogue<UP, Team<NT, 0>, -1, DBP_STATS_LA>(w, p, n, c, c + 1 == ncl, cl_first, tm);
       __syncthreads();
     }
   }
