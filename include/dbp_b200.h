@@ -109,6 +109,15 @@ int dbp_device_query(int* sm_count, int* cc_major, int* cc_minor, long long* l2_
 int dbp_gram_mrc(const void* H, const void* Y, int64_t n_items, int B, int u,
                  int u_stride, int T, int C, const int32_t* offsets,
                  int sum_clusters, void* stats, void* stream);
+/* dbp_gram_mrc with the split-bf16 part count of the tensor-core statistics
+ * kernels chosen by the caller: 0 = the default (3 parts, ~3xTF32), 2 = two
+ * parts (~2^-17 per Gram entry) -- for statistics that feed a well-conditioned
+ * PD solve (B >= 4 u), as the multi-GPU PD path uses it (the fused
+ * single-GPU PD kernel makes the same choice itself).  No reference
+ * counterpart beyond local_preprocess / centralized_stats (equalize.py:85-112). */
+int dbp_gram_mrc_parts(const void* H, const void* Y, int64_t n_items, int B, int u,
+                       int u_stride, int T, int C, const int32_t* offsets,
+                       int sum_clusters, int bf16_parts, void* stats, void* stream);
 
 /* Central equalization from fused statistics.  Replaces linear_equalize
  * (equalize.py:130-176) + unbiased_output (:179-195) for kind MRC/ZF/LMMSE,

@@ -39,6 +39,7 @@ SIGNATURES = {
     "dbp_set_option": [_i, _i],
     "dbp_device_query": [_vp, _vp, _vp, _vp],
     "dbp_gram_mrc": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp],
+    "dbp_gram_mrc_parts": [_vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp],
     "dbp_equalize_stats": [_vp, _i64, _i, _i, _i, _f, _vp, _i64, _f, _i, _f, _f, _i, _f,
                            _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "dbp_equalize": [_i, _i, _vp, _vp, _i64, _i, _i, _i, _i, _i, _vp, _vp, _i, _f, _vp, _i64,

@@ -53,6 +53,7 @@ struct EqParams {
   int ips, spi, stage_bytes, stage_hbytes, stage_ystride;
   int tc_simple, tc_bc;  // whole-item stages, full 32-row chunks, clusters of tc_bc rows
   int g_hermitian;       // G is the kernel's own Gram (exactly Hermitian in shared memory)
+  int nsplit;            // split-bf16 statistics: bf16 parts per operand (0: the kernel's default)
   int st_row0[MAX_SPI], st_rows[MAX_SPI];
   float* dbg_tile;  // debug: first operand tile of CTA 0 (DBP_TC_DUMP)
   long long* dbg;  // debug: per-role wait-cycle counters [5][4] (DBP_TC_DEBUG)

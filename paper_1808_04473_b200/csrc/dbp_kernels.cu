@@ -767,7 +767,13 @@ int dbp_device_query(int* sms, int* major, int* minor, long long* l2) {
 
 int dbp_gram_mrc(const void* H, const void* Y, int64_t n_items, int B, int u, int u_stride, int T, int C,
                  const int32_t* offsets, int sum_clusters, void* stats, void* stream) {
+  return dbp_gram_mrc_parts(H, Y, n_items, B, u, u_stride, T, C, offsets, sum_clusters, 0, stats, stream);
+}
+
+int dbp_gram_mrc_parts(const void* H, const void* Y, int64_t n_items, int B, int u, int u_stride, int T, int C,
+                       const int32_t* offsets, int sum_clusters, int bf16_parts, void* stats, void* stream) {
   if (n_items <= 0) return DBP_OK;
+  if (bf16_parts != 0 && bf16_parts != 2 && bf16_parts != 3) return fail(DBP_E_ARG, "bf16_parts must be 0, 2 or 3");
   if (!H || !Y || !stats || !offsets) return fail(DBP_E_ARG, "null pointer");
   EqParams q;
   memset(&q, 0, sizeof(q));
@@ -780,6 +786,7 @@ int dbp_gram_mrc(const void* H, const void* Y, int64_t n_items, int B, int u, in
   q.arch = ARCH_STATS;
   q.kind = EQ_MRC;
   q.sum_clusters = sum_clusters;
+  q.nsplit = bf16_parts;
   q.stats_out = static_cast<float2*>(stats);
   return dispatch_stream(q, static_cast<cudaStream_t>(stream));
 }

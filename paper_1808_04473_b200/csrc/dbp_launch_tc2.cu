@@ -113,7 +113,7 @@ int launch_tc2(EqParams& p, cudaStream_t st) {
   // parts kept x-hat at 1.1e-5 but tripled the boundary decision flips past the
   // 1e-5 rate bar -- and for the statistics API
   const bool two = p.arch != ARCH_STATS && (p.kind == EQ_MRC || (p.arch == ARCH_PD && K >= 4 * p.u));
-  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : two ? 2 : 3;
+  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : p.nsplit ? p.nsplit : two ? 2 : 3;
   if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
   const int raw = g.hbytes + g.ybox;
   g.stage_bytes = align_up(std::max(raw, nsplit * T2_SPLIT_BYTES), 1024);
@@ -203,7 +203,7 @@ int launch_tcw(EqParams& p, cudaStream_t st, int nsplit_default) {
   if ((p.us & 1) || (p.B & 1) || p.n_items > 0x7ffffff0) return 1;
   auto enc = tensor_map_encoder();
   if (!enc) return 1;
-  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : nsplit_default;
+  const int nsplit = opt(DBP_OPT_T2_NSPLIT) ? opt(DBP_OPT_T2_NSPLIT) : p.nsplit ? p.nsplit : nsplit_default;
   if (nsplit != 2 && nsplit != 3) return fail(DBP_E_ARG, "split count must be 2 or 3");
   TcwGeom g;
   memset(&g, 0, sizeof(g));

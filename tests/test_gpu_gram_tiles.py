@@ -66,3 +66,35 @@ def test_gram_mrc_tiles(n, b, u, t, offs, summed):
             assert np.abs(o[i, k, u * u:].reshape(t, u) - Z).max() < 2e-5 * scale_z, (i, k, "Z")
     if len(set(np.diff(offs))) == 1:  # uniform clusters run on the tensor cores (ragged: SIMT kernel)
         assert _lib.lib().dbp_last_kernel() in (_lib.KERNEL_TC_TF32, _lib.KERNEL_TC_BF16)
+
+
+def test_gram_mrc_parts_two_vs_three():
+    """dbp_gram_mrc_parts: two bf16 parts stay within ~2^-16 of the three-part
+    (~3xTF32) statistics on a well-conditioned PD geometry (the multi-GPU PD
+    path's choice), and 0 equals the default entry point bit for bit."""
+    import torch
+    from paper_1808_04473_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    n, b, c, u, t = 64, 128, 4, 16, 14
+    H = torch.tensor(((rng.standard_normal((n, b, u)) + 1j * rng.standard_normal((n, b, u))) / np.sqrt(2 * b))
+                     .astype(np.complex64), device="cuda")
+    Y = torch.tensor((rng.standard_normal((n, t, b)) + 1j * rng.standard_normal((n, t, b))).astype(np.complex64),
+                     device="cuda")
+    offs_keep, offs = _lib.host_i32(np.arange(0, b + 1, b // c))
+    lib = _lib.lib()
+    outs = {}
+    for parts in (0, 2, 3):
+        out = torch.empty((n, u * u + t * u), dtype=torch.complex64, device="cuda")
+        _lib.check(lib.dbp_gram_mrc_parts(_lib.ptr(H), _lib.ptr(Y), n, b, u, u, t, c, offs, 1, parts, _lib.ptr(out),
+                                          _lib.stream_ptr()))
+        outs[parts] = out.cpu().numpy()
+    ref = torch.empty((n, u * u + t * u), dtype=torch.complex64, device="cuda")
+    _lib.check(lib.dbp_gram_mrc(_lib.ptr(H), _lib.ptr(Y), n, b, u, u, t, c, offs, 1, _lib.ptr(ref), _lib.stream_ptr()))
+    assert np.array_equal(outs[0], ref.cpu().numpy())
+    assert np.array_equal(outs[0], outs[3])
+    scale = np.max(np.abs(outs[3]), axis=1, keepdims=True)
+    assert np.max(np.abs(outs[2] - outs[3]) / scale) < 2e-5
+    with pytest.raises(Exception):
+        _lib.check(lib.dbp_gram_mrc_parts(_lib.ptr(H), _lib.ptr(Y), n, b, u, u, t, c, offs, 1, 5, _lib.ptr(ref),
+                                          _lib.stream_ptr()))
