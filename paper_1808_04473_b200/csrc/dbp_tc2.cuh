@@ -770,14 +770,35 @@ __global__ void __launch_bounds__(32 * T2S_WARPS) t2_stats_solve_kernel(const __
       n0[k] = valid[k] ? item_n0(p, n[k]) : 0.f;
       if (!valid[k]) continue;
       const float2* src = p.stats_in + (size_t)n[k] * rec;
-      for (int e = lane; e < u * u; e += 32) {
-        const int i = e / u, j = e - i * u;
-        const float2 v = (i >= j) ? src[e] : c_conj(src[j * u + i]);
-        w[k].G[i * LD + j] = v;
-      }
-      for (int e = lane; e < T * 16; e += 32) {
-        const int t = e >> 4, i = e & 15;
-        w[k].Z[t * LD + i] = (i < u) ? src[u * u + t * u + i] : make_float2(0.f, 0.f);
+      if (!(u & 1) && !(reinterpret_cast<uintptr_t>(src) & 15)) {
+        // coalesced: the record's rows as float4 pairs, then the upper
+        // triangle mirrored from the lower one in shared memory
+        const int hu = u >> 1;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        for (int e = lane; e < (u + T) * hu; e += 32) {
+          const int r = e / hu, cc = 2 * (e - r * hu);
+          float2* dst = (r < u) ? w[k].G + r * LD + cc : w[k].Z + (r - u) * LD + cc;
+          *reinterpret_cast<float4*>(dst) = s4[e];
+        }
+        for (int e = lane; e < T * (16 - u); e += 32) {  // zero y past u (read by t2_solve_pair)
+          const int t = e / (16 - u), i = u + e - t * (16 - u);
+          w[k].Z[t * LD + i] = make_float2(0.f, 0.f);
+        }
+        __syncwarp();
+        for (int e = lane; e < u * u; e += 32) {
+          const int i = e / u, j = e - i * u;
+          if (i < j) w[k].G[i * LD + j] = c_conj(w[k].G[j * LD + i]);
+        }
+      } else {
+        for (int e = lane; e < u * u; e += 32) {
+          const int i = e / u, j = e - i * u;
+          const float2 v = (i >= j) ? src[e] : c_conj(src[j * u + i]);
+          w[k].G[i * LD + j] = v;
+        }
+        for (int e = lane; e < T * 16; e += 32) {
+          const int t = e >> 4, i = e & 15;
+          w[k].Z[t * LD + i] = (i < u) ? src[u * u + t * u + i] : make_float2(0.f, 0.f);
+        }
       }
     }
     __syncwarp();
