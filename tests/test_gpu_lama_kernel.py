@@ -85,3 +85,31 @@ def test_lama_kernel_per_item_noise_and_many_items():
         assert normwise_rel(det.xhat[pick], ref["z"]) < XHAT_TOL
         s2 = np.broadcast_to(det.sigma2[pick][:, :, None], ref["sigma2"].shape)
         assert entry_rel(s2, ref["sigma2"]) < SIGMA2_TOL
+
+
+@pytest.mark.parametrize("u", [24, 32])
+def test_lama_kernel_from_statistics_records(u):
+    """The multi-GPU PD central solve (dbp_equalize_stats without traces) runs
+    lama_kernel on the exchanged statistics, reading G by rows (as the
+    reference's i_minus_g @ s does): against the per-vector oracle."""
+    import torch
+
+    from paper_1808_04473_b200.distributed import CudaOps
+
+    const = dbp.make_constellation("qam16")
+    b, t, n = 4 * u, 14, 64
+    H, Y, _, n0 = synth_frames(11, 1, n, t, b, u, const, 9.0)
+    g = np.einsum("nbi,nbj->nij", H.conj().astype(complex), H.astype(complex))
+    ym = np.einsum("nbi,ntb->nti", H.conj().astype(complex), Y.astype(complex))
+    rec = np.concatenate([g.reshape(n, -1), ym.reshape(n, -1)], axis=1).astype(np.complex64)
+    ops = CudaOps("lama", u, t, const, lama_params={"t_max": 8})
+    beta = u / b
+    n0_items = torch.full((n,), float(n0[0]), dtype=torch.float32, device="cuda")
+    xhat, s2, dec, status, _ = ops.solve(torch.tensor(rec, device="cuda"), n0_items, beta)
+    assert int(status.abs().max()) == 0
+    xhat, s2 = xhat.cpu().numpy(), s2.cpu().numpy()
+    for i in range(0, n, 9):
+        for tt in range(t):
+            z, tau, _ = O.lama_equalize(g[i], ym[i, tt], const.symbols, const.es, float(n0[0]), beta, t_max=8)
+            assert normwise_rel(xhat[i, tt], z) < XHAT_TOL
+            assert entry_rel(s2[i, tt], tau[0]) < SIGMA2_TOL
