@@ -113,3 +113,24 @@ def test_lama_kernel_from_statistics_records(u):
             z, tau, _ = O.lama_equalize(g[i], ym[i, tt], const.symbols, const.es, float(n0[0]), beta, t_max=8)
             assert normwise_rel(xhat[i, tt], z) < XHAT_TOL
             assert entry_rel(s2[i, tt], tau[0]) < SIGMA2_TOL
+
+
+@pytest.mark.parametrize("arch", ["pd", "fd"])
+def test_lama_kernel_divergence_status(arch):
+    """A non-finite receive vector makes z^1 non-finite: DivergenceError at
+    iteration 1 for that item only (equalize.py:246-249), through the per-warp
+    status reduction of lama_kernel; the other items are unaffected."""
+    from paper_1808_04473_b200 import DivergenceError
+
+    const = dbp.make_constellation("qam16")
+    counts = [32] * 4
+    H, Y, _, n0 = synth_frames(5, 1, 40, 14, 128, 32, const, 10.0)
+    Y = Y.copy()
+    Y[7, 3, 5] = np.nan
+    with pytest.raises(DivergenceError) as err:
+        dbp.detect(arch, "lama", H, Y, n0[0], counts, const, lama_params={"t_max": 5})
+    assert err.value.iteration == 1
+    assert "item 7" in str(err.value)
+    det = dbp.detect(arch, "lama", H, Y, n0[0], counts, const, lama_params={"t_max": 5}, check=False)
+    st = np.asarray(det.status)
+    assert st[7] == _lib.ST_DIVERGED and np.count_nonzero(st) == 1
