@@ -294,7 +294,12 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
       m[r][c] = v;
     }
   __syncthreads();  // G is scratch from here on
+  // Rt rows are stored column-permuted: columns {4t, 4t+1} at 2t, columns
+  // {4t+2, 4t+3} at 32 + 2t, so the eight lanes of a quarter-warp read eight
+  // consecutive 16-byte chunks (conflict-free; the natural order put two of
+  // them on each bank group: 2x the wavefronts on the update's hottest loads)
   float2* rt = w.G;                                  // [2][8][64]  Rt of the step (block parity)
+  auto rtc = [](int j) { return ((j >> 2) << 1) + ((j & 2) << 4) + (j & 1); };
   float2* pinvb = w.G + 2 * 512;                     // [2][8][8]   Pinv of the step (look-ahead)
   float2* cb = w.G + 2 * 512 + 2 * 64 + warp * 192;  // per warp: C [8][8], Ct [8][8], own Pinv [8][8]
   float2* ctb = cb + 64;
@@ -314,8 +319,8 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
         v[c] = m[r][c];
         if (4 * tj + c == 8 * b + lr) v[c].x += 1.f;
       }
-      *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
-      *reinterpret_cast<float4*>(rb + lr * 64 + 4 * tj + 2) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+      *reinterpret_cast<float4*>(rb + lr * 64 + 2 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+      *reinterpret_cast<float4*>(rb + lr * 64 + 32 + 2 * tj) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
     }
   };
   // Pinv_b = (Rt_b[:, K] - I)^-1 into pb (one warp)
@@ -323,7 +328,8 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
     const float2* rb = rt + (b & 1) * 512;
     // lane l holds P[pr][pc], P[pr + 1][pc] (pr = 2 (l / 8), pc = l % 8)
     const int pc = lane & 7, pr = 2 * (lane >> 3);
-    float2 q0 = rb[pr * 64 + 8 * b + pc], q1 = rb[(pr + 1) * 64 + 8 * b + pc];
+    const int pcol = rtc(8 * b + pc);
+    float2 q0 = rb[pr * 64 + pcol], q1 = rb[(pr + 1) * 64 + pcol];
     if (pr == pc) q0.x -= 1.f;
     if (pr + 1 == pc) q1.x -= 1.f;
 #pragma unroll
@@ -409,8 +415,8 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const float4 v0 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 4 * tj);
-        const float4 v1 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 4 * tj + 2);
+        const float4 v0 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 2 * tj);
+        const float4 v1 = *reinterpret_cast<const float4*>(rb + (l + e) * 64 + 32 + 2 * tj);
         rr[e][0] = make_float2(v0.x, v0.y);
         rr[e][1] = make_float2(v0.z, v0.w);
         rr[e][2] = make_float2(v1.x, v1.y);
