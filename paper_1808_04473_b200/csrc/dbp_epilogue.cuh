@@ -277,22 +277,51 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
   const int LD = w.LD;
   const int ti = tid >> 4, tj = tid & 15, warp = tid >> 5, lane = tid & 31;
   float2 m[4][4];
+  // the tile's two 16-byte halves per row, the lanes with (tj / 4) odd taking
+  // the second half first: the eight lanes of a quarter-warp then touch eight
+  // distinct bank groups (the element-wise loads were 4-way conflicted)
+  const bool swp = (tj >> 2) & 1;
+  if (u == 64) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 4; ++r) {
+      const int i = 4 * ti + r;
+      const float2* row = w.G + i * LD + 4 * tj;
+      const float4 a0 = *reinterpret_cast<const float4*>(row + (swp ? 2 : 0));
+      const float4 a1 = *reinterpret_cast<const float4*>(row + (swp ? 0 : 2));
+      const float4 lo = swp ? a1 : a0, hi = swp ? a0 : a1;
+      m[r][0] = make_float2(lo.x, lo.y);
+      m[r][1] = make_float2(lo.z, lo.w);
+      m[r][2] = make_float2(hi.x, hi.y);
+      m[r][3] = make_float2(hi.z, hi.w);
+    }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = 4 * ti + r, j = 4 * tj + c;
-      float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
-      if (i < u && j < u) {
-        v = w.G[i * LD + j];
-        if (i == j) {
-          v.x += rho;
-          v.y = 0.f;
-          w.dg[i] = v.x;
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (4 * ti + r == 4 * tj + c) {
+          m[r][c].x += rho;
+          m[r][c].y = 0.f;
+          w.dg[4 * ti + r] = m[r][c].x;
         }
       }
-      m[r][c] = v;
-    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * ti + r, j = 4 * tj + c;
+        float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
+        if (i < u && j < u) {
+          v = w.G[i * LD + j];
+          if (i == j) {
+            v.x += rho;
+            v.y = 0.f;
+            w.dg[i] = v.x;
+          }
+        }
+        m[r][c] = v;
+      }
+  }
   __syncthreads();  // G is scratch from here on
   // Rt rows are stored column-permuted: columns {4t, 4t+1} at 2t, columns
   // {4t+2, 4t+3} at 32 + 2t, so the eight lanes of a quarter-warp read eight
@@ -442,6 +471,17 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(w.flags, ST_SINGULAR);
   // (the last barrier of the loop: every scratch read is done)
+  if (u == 64) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float2* row = w.G + (4 * ti + r) * LD + 4 * tj;
+      const float4 lo = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
+      const float4 hi = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
+      *reinterpret_cast<float4*>(row + (swp ? 2 : 0)) = swp ? hi : lo;
+      *reinterpret_cast<float4*>(row + (swp ? 0 : 2)) = swp ? lo : hi;
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int i = 4 * ti + r;
