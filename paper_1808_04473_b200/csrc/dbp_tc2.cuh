@@ -340,22 +340,47 @@ __device__ __forceinline__ void t2_gj2d(float2* Gw, int LD, int u, float rho, bo
   const int h16 = lane & 16, bi = (lane >> 2) & 3, bj = lane & 3;
   float2 m[4][4];
   float dgl[4];
+  // full units: the block's rows as two 16-byte halves, lanes with bi odd
+  // taking the second half first, so a quarter-warp's eight lanes hit eight
+  // distinct bank groups (element-wise loads / stores were 4-way conflicted)
+  const bool full = act && u == 16, swp = bi & 1;
+  if (full) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < 4; ++r) {
+      const float2* row = Gw + (4 * bi + r) * LD + 4 * bj;
+      const float4 a0 = *reinterpret_cast<const float4*>(row + (swp ? 2 : 0));
+      const float4 a1 = *reinterpret_cast<const float4*>(row + (swp ? 0 : 2));
+      const float4 lo = swp ? a1 : a0, hi = swp ? a0 : a1;
+      m[r][0] = make_float2(lo.x, lo.y);
+      m[r][1] = make_float2(lo.z, lo.w);
+      m[r][2] = make_float2(hi.x, hi.y);
+      m[r][3] = make_float2(hi.z, hi.w);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = 4 * bi + r, jj = 4 * bj + c;
-      float2 v = make_float2(i == jj ? 1.f : 0.f, 0.f);
-      if (act && i < u && jj < u) {
-        v = Gw[i * LD + jj];
-        if (i == jj) {
-          v.x += rho;
-          v.y = 0.f;
+      for (int c = 0; c < 4; ++c)
+        if (bi == bj && r == c) {
+          m[r][c].x += rho;
+          m[r][c].y = 0.f;
         }
-      }
-      m[r][c] = v;
+      dgl[r] = m[r][r].x;  // the original diagonal (meaningful on the diagonal lanes bi == bj)
     }
-    dgl[r] = m[r][r].x;  // the original diagonal (meaningful on the diagonal lanes bi == bj)
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * bi + r, jj = 4 * bj + c;
+        float2 v = make_float2(i == jj ? 1.f : 0.f, 0.f);
+        if (act && i < u && jj < u) {
+          v = Gw[i * LD + jj];
+          if (i == jj) {
+            v.x += rho;
+            v.y = 0.f;
+          }
+        }
+        m[r][c] = v;
+      }
+      dgl[r] = m[r][r].x;  // the original diagonal (meaningful on the diagonal lanes bi == bj)
+    }
   }
   const float tolf = 8.f * (float)u * FLT_EPSILON;
   const int nkb = (u + 3) >> 2;
@@ -388,6 +413,17 @@ __device__ __forceinline__ void t2_gj2d(float2* Gw, int LD, int u, float rho, bo
 #pragma unroll
         for (int c = 0; c < 4; ++c) c_fms2(m[r][c], cr[r], rr[c]);
     }
+  }
+  if (full) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float2* row = Gw + (4 * bi + r) * LD + 4 * bj;
+      const float4 lo = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
+      const float4 hi = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
+      *reinterpret_cast<float4*>(row + (swp ? 2 : 0)) = swp ? hi : lo;
+      *reinterpret_cast<float4*>(row + (swp ? 0 : 2)) = swp ? lo : hi;
+    }
+    return;
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r)
