@@ -638,6 +638,48 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
   // the A row; rows are 16-byte aligned (LD even) -> float4 loads
   const bool unb = (a.kind == EQ_LMMSE) && a.unbias;
   const int th = (T + 1) / 2;
+  if (UP == 64 && !(u & 1)) {
+    // 2 x 2 register tiles: rows ip, ip + u/2 and symbols t0, t0 + th share
+    // each A-row / y load (4 float4 loads per 8 complex MACs instead of 3 per 4;
+    // U = 64 only: at UP = 32 the tiles cost stats_kernel<32> its second CTA per SM)
+    const int hu = u >> 1;
+    for (int e = tid; e < th * hu; e += NT) {
+      const int t0 = e / hu, ip = e - t0 * hu;
+      const int t1 = t0 + th;
+      const float2* ar0 = w.G + ip * LD;
+      const float2* ar1 = w.G + (ip + hu) * LD;
+      const float2* z0 = w.Z + t0 * LD;
+      const float2* z1 = w.Z + (t1 < T ? t1 : t0) * LD;
+      float2 c00 = make_float2(0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;  // [row][symbol]
+      for (int jj = 0; jj < u; jj += 2) {
+        const float4 a0 = *reinterpret_cast<const float4*>(ar0 + jj);
+        const float4 a1 = *reinterpret_cast<const float4*>(ar1 + jj);
+        const float4 b0 = *reinterpret_cast<const float4*>(z0 + jj);
+        const float4 b1 = *reinterpret_cast<const float4*>(z1 + jj);
+        c_fma2(c00, make_float2(a0.x, a0.y), make_float2(b0.x, b0.y));
+        c_fma2(c01, make_float2(a0.x, a0.y), make_float2(b1.x, b1.y));
+        c_fma2(c10, make_float2(a1.x, a1.y), make_float2(b0.x, b0.y));
+        c_fma2(c11, make_float2(a1.x, a1.y), make_float2(b1.x, b1.y));
+        c_fma2(c00, make_float2(a0.z, a0.w), make_float2(b0.z, b0.w));
+        c_fma2(c01, make_float2(a0.z, a0.w), make_float2(b1.z, b1.w));
+        c_fma2(c10, make_float2(a1.z, a1.w), make_float2(b0.z, b0.w));
+        c_fma2(c11, make_float2(a1.z, a1.w), make_float2(b1.z, b1.w));
+      }
+      if (unb) {
+        const float rc0 = 1.f / (1.f - rho * ar0[ip].x), rc1 = 1.f / (1.f - rho * ar1[ip + hu].x);
+        c00 = c_scale(c00, rc0);
+        c01 = c_scale(c01, rc0);
+        c10 = c_scale(c10, rc1);
+        c11 = c_scale(c11, rc1);
+      }
+      w.X[t0 * LD + ip] = c00;
+      w.X[t0 * LD + ip + hu] = c10;
+      if (t1 < T) {
+        w.X[t1 * LD + ip] = c01;
+        w.X[t1 * LD + ip + hu] = c11;
+      }
+    }
+  } else
   for (int e = tid; e < th * u; e += NT) {
     const int t0 = e / u, i = e - t0 * u;
     const int t1 = t0 + th;

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 #define DBP_STATS64_MINB 3
 #endif
 template <int UP, int NT>
-__global__ void __launch_bounds__(NT, (UP == 64 ? DBP_STATS64_MINB : 1)) stats_kernel(const __grid_constant__ EqParams p) {
+__global__ void __launch_bounds__(NT, (UP == 64 ? DBP_STATS64_MINB : 512 / NT)) stats_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
   const bool lama = p.kind == EQ_LAMA;
