@@ -495,6 +495,227 @@ __device__ __forceinline__ void gj64_blocked(const Work& w, int u, float rho, in
   }
 }
 
+// The same blocked sweep on a 128-thread team with 8 x 4 tiles: thread
+// (ti, tj), ti = tid / 16 in [0, 8), tj = tid % 16, holds rows 8 ti .. 8 ti + 7
+// (pivot block ti) x cols 4 tj .. 4 tj + 3; warp w owns pivot blocks 2w, 2w + 1.
+// Per pivot column l of the rank-8 update a thread reads its block's 8 Ct
+// values (stored transposed: one broadcast float4 run per quarter-warp) and 4
+// Rt values: 12 words per 32 complex MACs (5.3 FMA per word; the 4 x 4 tiles
+// of gj64_blocked: 4), and four items share an SM.
+template <bool lookahead>
+__device__ __forceinline__ void gj64_8x4(const Work& w, int u, float rho, int tid) {
+  const int LD = w.LD;
+  const int ti = tid >> 4, tj = tid & 15, warp = tid >> 5, lane = tid & 31;
+  float2 m[8][4];
+  const bool swp = (tj >> 2) & 1;  // rotated 16-byte halves: conflict-free quarter-warps
+  if (u == 64) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float2* row = w.G + (8 * ti + r) * LD + 4 * tj;
+      const float4 a0 = *reinterpret_cast<const float4*>(row + (swp ? 2 : 0));
+      const float4 a1 = *reinterpret_cast<const float4*>(row + (swp ? 0 : 2));
+      const float4 lo = swp ? a1 : a0, hi = swp ? a0 : a1;
+      m[r][0] = make_float2(lo.x, lo.y);
+      m[r][1] = make_float2(lo.z, lo.w);
+      m[r][2] = make_float2(hi.x, hi.y);
+      m[r][3] = make_float2(hi.z, hi.w);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (8 * ti + r == 4 * tj + c) {
+          m[r][c].x += rho;
+          m[r][c].y = 0.f;
+          w.dg[8 * ti + r] = m[r][c].x;
+        }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 8 * ti + r, j = 4 * tj + c;
+        float2 v = make_float2(i == j ? 1.f : 0.f, 0.f);  // padding: identity
+        if (i < u && j < u) {
+          v = w.G[i * LD + j];
+          if (i == j) {
+            v.x += rho;
+            v.y = 0.f;
+            w.dg[i] = v.x;
+          }
+        }
+        m[r][c] = v;
+      }
+  }
+  __syncthreads();  // G is scratch from here on
+  // Rt rows column-permuted as in gj64_blocked (conflict-free quarter-warps)
+  float2* rt = w.G;                                   // [2][8][64]  Rt of the step (block parity)
+  auto rtc = [](int j) { return ((j >> 2) << 1) + ((j & 2) << 4) + (j & 1); };
+  float2* pinvb = w.G + 2 * 512;                      // [2][8][8]   Pinv of the step (look-ahead)
+  float2* cb = w.G + 2 * 512 + 2 * 64 + warp * 320;   // per warp: C [16][8], Ct^T [8][16], own Pinv [8][8]
+  float2* ctT = cb + 128;
+  float2* pown = cb + 256;
+  const float tolf = 8.f * (float)u * FLT_EPSILON;
+  const int nblk = (u + 7) >> 3;
+  bool bad = false;
+  auto publish = [&](int b) {  // the 16 threads of block b's rows
+    if (ti != b) return;
+    float2* rb = rt + (b & 1) * 512;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float2 v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        v[c] = m[r][c];
+        if (4 * tj + c == 8 * b + r) v[c].x += 1.f;
+      }
+      *reinterpret_cast<float4*>(rb + r * 64 + 2 * tj) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+      *reinterpret_cast<float4*>(rb + r * 64 + 32 + 2 * tj) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+    }
+  };
+  auto invert = [&](int b, float2* pb) {  // Pinv_b = (Rt_b[:, K] - I)^-1 (one warp)
+    const float2* rb = rt + (b & 1) * 512;
+    const int pc = lane & 7, pr = 2 * (lane >> 3);
+    const int pcol = rtc(8 * b + pc);
+    float2 q0 = rb[pr * 64 + pcol], q1 = rb[(pr + 1) * 64 + pcol];
+    if (pr == pc) q0.x -= 1.f;
+    if (pr + 1 == pc) q1.x -= 1.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int src_col = (pr >> 1) * 8 + k;
+      const int src_row = (k >> 1) * 8 + pc;
+      const int src_piv = (k >> 1) * 8 + k;
+      const float c0x = __shfl_sync(0xffffffffu, q0.x, src_col), c0y = __shfl_sync(0xffffffffu, q0.y, src_col);
+      const float c1x = __shfl_sync(0xffffffffu, q1.x, src_col), c1y = __shfl_sync(0xffffffffu, q1.y, src_col);
+      const float rkx = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_row);
+      const float rky = __shfl_sync(0xffffffffu, (k & 1) ? q1.y : q0.y, src_row);
+      float p = __shfl_sync(0xffffffffu, (k & 1) ? q1.x : q0.x, src_piv);
+      const int kg = 8 * b + k;
+      if (kg < u && !(p > tolf * w.dg[kg])) {
+        bad = true;
+        p = 1.f;
+      }
+      const float rp = rcp_pivot(p);
+      const float2 rj = (pc == k) ? make_float2(1.f + rp, 0.f) : make_float2(rkx * rp, rky * rp);
+      const float2 ci0 = (pr == k) ? make_float2(p - 1.f, 0.f) : make_float2(c0x, c0y);
+      const float2 ci1 = (pr + 1 == k) ? make_float2(p - 1.f, 0.f) : make_float2(c1x, c1y);
+      c_fms(q0, ci0, rj);
+      c_fms(q1, ci1, rj);
+    }
+    pb[pr * 8 + pc] = q0;
+    pb[(pr + 1) * 8 + pc] = q1;
+  };
+  if (warp == 0) {
+    publish(0);
+    if constexpr (lookahead) {
+      __syncwarp();
+      invert(0, pinvb);
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b) {
+    const float2* rb = rt + (b & 1) * 512;
+    const float2* pb = pinvb + (b & 1) * 64;
+    if constexpr (!lookahead) {
+      invert(b, pown);
+      pb = pown;
+    }
+    // this warp's 16 rows of the pivot columns (threads holding columns 8b..8b+7)
+    if ((tj >> 1) == b) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int lr = 8 * (ti & 1) + r, c0 = 4 * (tj & 1);
+        *reinterpret_cast<float4*>(cb + lr * 8 + c0) = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
+        *reinterpret_cast<float4*>(cb + lr * 8 + c0 + 2) = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
+      }
+    }
+    __syncwarp();
+    // Ct^T for the warp's rows: lane -> row lr = lane / 2, columns 4 (lane % 2) + {0..3};
+    // the pivot block's own rows take I - Pinv
+    {
+      const int lr = lane >> 1, c0 = 4 * (lane & 1);
+      float2 a[4];
+      if ((b >> 1) == warp && (lr >> 3) == (b & 1)) {
+        const int rl = lr & 7;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float2 pv = pb[rl * 8 + c0 + c];
+          a[c] = make_float2((rl == c0 + c ? 1.f : 0.f) - pv.x, -pv.y);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[c] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const float2 cv = cb[lr * 8 + l];
+          const float4 p0 = *reinterpret_cast<const float4*>(pb + l * 8 + c0);
+          const float4 p1 = *reinterpret_cast<const float4*>(pb + l * 8 + c0 + 2);
+          c_fma2(a[0], cv, make_float2(p0.x, p0.y));
+          c_fma2(a[1], cv, make_float2(p0.z, p0.w));
+          c_fma2(a[2], cv, make_float2(p1.x, p1.y));
+          c_fma2(a[3], cv, make_float2(p1.z, p1.w));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ctT[(c0 + c) * 16 + lr] = a[c];
+    }
+    __syncwarp();
+    // rank-8 update of the tile
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      float2 cr[8], rr[4];
+      const float2* cl = ctT + l * 16 + 8 * (ti & 1);
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) {
+        const float4 v = *reinterpret_cast<const float4*>(cl + r);
+        cr[r] = make_float2(v.x, v.y);
+        cr[r + 1] = make_float2(v.z, v.w);
+      }
+      const float4 v0 = *reinterpret_cast<const float4*>(rb + l * 64 + 2 * tj);
+      const float4 v1 = *reinterpret_cast<const float4*>(rb + l * 64 + 32 + 2 * tj);
+      rr[0] = make_float2(v0.x, v0.y);
+      rr[1] = make_float2(v0.z, v0.w);
+      rr[2] = make_float2(v1.x, v1.y);
+      rr[3] = make_float2(v1.z, v1.w);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) c_fms2(m[r][c], cr[r], rr[c]);
+    }
+    __syncwarp();  // the warp's Ct / C / Pinv reads are done before the next block rewrites them
+    if (warp == ((b + 1) >> 1) && b + 1 < nblk) {
+      publish(b + 1);
+      if constexpr (lookahead) {
+        __syncwarp();
+        invert(b + 1, pinvb + ((b + 1) & 1) * 64);
+      }
+    }
+    __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) set_status(w.flags, ST_SINGULAR);
+  if (u == 64) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float2* row = w.G + (8 * ti + r) * LD + 4 * tj;
+      const float4 lo = make_float4(m[r][0].x, m[r][0].y, m[r][1].x, m[r][1].y);
+      const float4 hi = make_float4(m[r][2].x, m[r][2].y, m[r][3].x, m[r][3].y);
+      *reinterpret_cast<float4*>(row + (swp ? 2 : 0)) = swp ? hi : lo;
+      *reinterpret_cast<float4*>(row + (swp ? 0 : 2)) = swp ? lo : hi;
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = 8 * ti + r;
+    if (i < u) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = 4 * tj + c;
+        if (j < u) w.G[i * LD + j] = m[r][c];
+      }
+    }
+  }
+}
+
 // ---- linear equalizers on (G, Z) -> X (per symbol), s2, gn --------------
 // equalize.py:130-176 (+ unbiased_output :179-195 when a.unbias).
 //  MRC  : d = Re G_ii; z = y/d; s2 = N0/d + Es sum_{j!=i}|G_ij|^2/d^2
@@ -543,6 +764,8 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
   }
   if constexpr (UP == 64 && NT == 256) {
     gj64_blocked<LA>(w, u, rho, tid);  // eight pivots per barrier
+  } else if constexpr (UP == 64 && NT == 128) {
+    gj64_8x4<LA>(w, u, rho, tid);  // 8 x 4 tiles, 128-thread team
   } else {
     // thread -> elements (i0 + r*RS, j): fixed column, RS-strided rows.  The
     // sweep is the branch-free rank-1 update of linear_solve_warp_n

@@ -327,10 +327,10 @@ __global__ void __launch_bounds__(NT) stream_kernel(const __grid_constant__ EqPa
 #define DBP_STATS_LA true  // U = 64 solve: look-ahead pivot-block inversion on one warp
 #endif
 #ifndef DBP_STATS64_MINB
-#define DBP_STATS64_MINB 3
+#define DBP_STATS64_MINB 3  // U = 64, 256-thread team (4 x 4 tiles); the 128-thread team (8 x 4) runs four per SM
 #endif
 template <int UP, int NT>
-__global__ void __launch_bounds__(NT, (UP == 64 ? DBP_STATS64_MINB : 512 / NT)) stats_kernel(const __grid_constant__ EqParams p) {
+__global__ void __launch_bounds__(NT, (UP == 64 ? (NT == 128 ? 4 : DBP_STATS64_MINB) : 512 / NT)) stats_kernel(const __grid_constant__ EqParams p) {
   extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
   const bool lama = p.kind == EQ_LAMA;
