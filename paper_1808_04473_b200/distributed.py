@@ -558,7 +558,9 @@ def bench_main(args, wl, name, bench):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c64 (fp32 arithmetic)",
             "data": "synthetic i.i.d. Rayleigh, generated on the GPU (dbp_synthesize, seeded)",
-            "config": bench.config_dict(name, wl2, par),
+            "config": dict(bench.config_dict(name, wl2, par),
+                           l2=f"inputs {(Hd.numel() + Yd.numel()) * 8 / 2**20:.0f} MiB/step per rank vs 126 MiB L2; "
+                              f"one input set"),
             "roofline": {"bound": "hbm", "achieved": hbm / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": hbm / (ms * 1e-3) / 1e9 / hbm_peak, "traffic": None,
                          "algorithmic_bytes_per_launch": hbm, "per": "rank",
