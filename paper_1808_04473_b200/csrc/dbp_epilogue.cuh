@@ -733,7 +733,7 @@ __device__ __forceinline__ void gj64_8x4(const Work& w, int u, float rho, int ti
 // rounding noise ~eps*G_jj instead of an exact zero).
 // LA: the blocked U = 64 solve inverts each pivot block on one warp (look-ahead;
 // for kernels with two CTAs per SM), else on every warp
-template <int UP, class TM, bool LA = false>
+template <int UP, class TM, bool LA = false, bool XZ = false>
 __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
   constexpr int NT = TM::N;
   const int tid = tm.t;
@@ -866,14 +866,17 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
     // each A-row / y load (4 float4 loads per 8 complex MACs instead of 3 per 4;
     // U = 64 only: at UP = 32 the tiles cost stats_kernel<32> its second CTA per SM)
     const int hu = u >> 1;
-    for (int e = tid; e < th * hu; e += NT) {
+    auto tile = [&](int e, float2& c00, float2& c01, float2& c10, float2& c11) {
       const int t0 = e / hu, ip = e - t0 * hu;
       const int t1 = t0 + th;
       const float2* ar0 = w.G + ip * LD;
       const float2* ar1 = w.G + (ip + hu) * LD;
       const float2* z0 = w.Z + t0 * LD;
       const float2* z1 = w.Z + (t1 < T ? t1 : t0) * LD;
-      float2 c00 = make_float2(0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;  // [row][symbol]
+      c00 = make_float2(0.f, 0.f);  // [row][symbol]
+      c01 = c00;
+      c10 = c00;
+      c11 = c00;
       for (int jj = 0; jj < u; jj += 2) {
         const float4 a0 = *reinterpret_cast<const float4*>(ar0 + jj);
         const float4 a1 = *reinterpret_cast<const float4*>(ar1 + jj);
@@ -895,11 +898,32 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
         c10 = c_scale(c10, rc1);
         c11 = c_scale(c11, rc1);
       }
+    };
+    auto put = [&](int e, float2 c00, float2 c01, float2 c10, float2 c11) {
+      const int t0 = e / hu, ip = e - t0 * hu;
+      const int t1 = t0 + th;
       w.X[t0 * LD + ip] = c00;
       w.X[t0 * LD + ip + hu] = c10;
       if (t1 < T) {
         w.X[t1 * LD + ip] = c01;
         w.X[t1 * LD + ip + hu] = c11;
+      }
+    };
+    if constexpr (XZ) {  // X overwrites y_mrc (make_work_layout x_in_z, T <= 16): tiles held across a barrier
+      constexpr int MAXE = (8 * 32 + NT - 1) / NT;
+      float2 hold[MAXE][4];
+#pragma unroll
+      for (int k = 0; k < MAXE; ++k)
+        if (tid + k * NT < th * hu) tile(tid + k * NT, hold[k][0], hold[k][1], hold[k][2], hold[k][3]);
+      tm.sync();
+#pragma unroll
+      for (int k = 0; k < MAXE; ++k)
+        if (tid + k * NT < th * hu) put(tid + k * NT, hold[k][0], hold[k][1], hold[k][2], hold[k][3]);
+    } else {
+      for (int e = tid; e < th * hu; e += NT) {
+        float2 c00, c01, c10, c11;
+        tile(e, c00, c01, c10, c11);
+        put(e, c00, c01, c10, c11);
       }
     }
   } else
@@ -1197,7 +1221,7 @@ __device__ __forceinline__ void write_status(const Work& w, const EqParams& p, i
 // CLS: equalizer class known at compile time (0 stats only, 1 linear, 2 LAMA)
 // so a kernel instantiated for one class carries no code of the others; -1
 // decides at run time (SIMT kernels).
-template <int UP, class TM, int CLS = -1, bool LA = false>
+template <int UP, class TM, int CLS = -1, bool LA = false, bool XZ = false>
 __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int cluster, bool item_end,
                               int& cl_first, const TM& tm, long long* dbg_solve = nullptr,
                               float n0_pre = -1.f) {
@@ -1253,7 +1277,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
       lama_unit<UP>(w, a, p.cp, tz, ts, tv, tp, tm, p.g_hermitian != 0);
     } else {
       const long long t0 = dbg_solve ? clock64() : 0;
-      linear_unit<UP, TM, LA>(w, a, tm);
+      linear_unit<UP, TM, LA, XZ>(w, a, tm);
       if (dbg_solve) *dbg_solve += clock64() - t0;
     }
     if (u == UP) {  // shifts instead of divisions
@@ -1293,7 +1317,7 @@ __device__ void unit_epilogue(const Work& w, const EqParams& p, int64_t n, int c
   if (lama)
     lama_unit<UP>(w, a, p.cp, nullptr, nullptr, nullptr, nullptr, tm, p.g_hermitian != 0);
   else
-    linear_unit<UP, TM, LA>(w, a, tm);
+    linear_unit<UP, TM, LA, XZ>(w, a, tm);
   // weights: MRC -> Gram diagonal (fusion.py:149-151), otherwise
   // 1/max(sigma2, 1e-15) (fusion.py:96-105); sigma2 <= 0 is a ConfigError
   const int wdim = lama ? T : u;

@@ -53,12 +53,12 @@ static int launch_stream(EqParams& p, cudaStream_t st) {
   return cuda_check("stream_kernel");
 }
 
-template <int UP, int NT>
+template <int UP, int NT, bool XZ = false>
 static int launch_stats(EqParams& p, cudaStream_t st) {
   const bool lama = p.kind == EQ_LAMA;
   const bool fd = p.arch == ARCH_FD;
-  const WorkLayout L = make_work_layout(0, UP, p.TP, fd ? p.C : 1, lama, fd);
-  auto kern = stats_kernel<UP, NT>;
+  const WorkLayout L = make_work_layout(0, UP, p.TP, fd ? p.C : 1, lama, fd, XZ);
+  auto kern = stats_kernel<UP, NT, XZ>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
     return fail(DBP_E_CUDA, "shared memory request too large");
   int per_sm = 0;
@@ -84,10 +84,12 @@ int launch_stats_up(int up, EqParams& p, cudaStream_t st) {
     case 8: return launch_stats<8, 128>(p, st);
     case 16: return launch_stats<16, 128>(p, st);
     case 32: return launch_stats<32, 256>(p, st);
-    // U = 64 solves: 128-thread teams with 8 x 4 tiles for one record per item
-    // (PD: cfg5-pd512 11.9 -> 11.6 ms); FD's C sequential cluster solves and
-    // folds per item keep the 256-thread team (measured 1.3 % faster there)
-    case 64: return p.arch == ARCH_FD ? launch_stats<64, 256>(p, st) : launch_stats<64, 128>(p, st);
+    // U = 64 solves: 128-thread teams with 8 x 4 tiles, four per SM (PD:
+    // cfg5-pd512 11.9 -> 11.6 ms); FD linear solves fit four per SM with X in Z
+    // (FD LAMA / odd u keep the 256-thread team)
+    case 64:
+      if (p.arch != ARCH_FD) return launch_stats<64, 128>(p, st);
+      return stats_x_in_z(p) ? launch_stats<64, 128, true>(p, st) : launch_stats<64, 256>(p, st);
   }
   return fail(DBP_E_UNSUPPORTED, "u must be <= 64");
 }
