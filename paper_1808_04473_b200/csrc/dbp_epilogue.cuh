@@ -910,15 +910,64 @@ __device__ void linear_unit(const Work& w, const EpiArgs& a, const TM& tm) {
       }
     };
     if constexpr (XZ) {  // X overwrites y_mrc (make_work_layout x_in_z, T <= 16): tiles held across a barrier
-      constexpr int MAXE = (8 * 32 + NT - 1) / NT;
-      float2 hold[MAXE][4];
+      static_assert(NT == 128, "X in Z: two 2 x 2 tiles per thread of a 128-thread team");
+      // both tiles of the thread in one pass (th * hu <= 256 = 2 NT); a missing
+      // second tile recomputes the first and is not stored
+      const int e0 = tid, e1 = (tid + NT < th * hu) ? tid + NT : tid;
+      const int t0a = e0 / hu, ipa = e0 - t0a * hu, t0b = e1 / hu, ipb = e1 - t0b * hu;
+      const float2* ra0 = w.G + ipa * LD;
+      const float2* ra1 = w.G + (ipa + hu) * LD;
+      const float2* rb0 = w.G + ipb * LD;
+      const float2* rb1 = w.G + (ipb + hu) * LD;
+      const float2* za0 = w.Z + t0a * LD;
+      const float2* za1 = w.Z + (t0a + th < T ? t0a + th : t0a) * LD;
+      const float2* zb0 = w.Z + t0b * LD;
+      const float2* zb1 = w.Z + (t0b + th < T ? t0b + th : t0b) * LD;
+      float2 ha[4], hb[4];
 #pragma unroll
-      for (int k = 0; k < MAXE; ++k)
-        if (tid + k * NT < th * hu) tile(tid + k * NT, hold[k][0], hold[k][1], hold[k][2], hold[k][3]);
+      for (int q = 0; q < 4; ++q) ha[q] = hb[q] = make_float2(0.f, 0.f);
+      const bool live0 = e0 < th * hu;
+      for (int jj = 0; jj < u; jj += 2) {
+        const float4 a0 = *reinterpret_cast<const float4*>(ra0 + jj);
+        const float4 a1 = *reinterpret_cast<const float4*>(ra1 + jj);
+        const float4 b0 = *reinterpret_cast<const float4*>(za0 + jj);
+        const float4 b1 = *reinterpret_cast<const float4*>(za1 + jj);
+        const float4 c0 = *reinterpret_cast<const float4*>(rb0 + jj);
+        const float4 c1 = *reinterpret_cast<const float4*>(rb1 + jj);
+        const float4 d0 = *reinterpret_cast<const float4*>(zb0 + jj);
+        const float4 d1 = *reinterpret_cast<const float4*>(zb1 + jj);
+        c_fma2(ha[0], make_float2(a0.x, a0.y), make_float2(b0.x, b0.y));
+        c_fma2(ha[1], make_float2(a0.x, a0.y), make_float2(b1.x, b1.y));
+        c_fma2(ha[2], make_float2(a1.x, a1.y), make_float2(b0.x, b0.y));
+        c_fma2(ha[3], make_float2(a1.x, a1.y), make_float2(b1.x, b1.y));
+        c_fma2(ha[0], make_float2(a0.z, a0.w), make_float2(b0.z, b0.w));
+        c_fma2(ha[1], make_float2(a0.z, a0.w), make_float2(b1.z, b1.w));
+        c_fma2(ha[2], make_float2(a1.z, a1.w), make_float2(b0.z, b0.w));
+        c_fma2(ha[3], make_float2(a1.z, a1.w), make_float2(b1.z, b1.w));
+        c_fma2(hb[0], make_float2(c0.x, c0.y), make_float2(d0.x, d0.y));
+        c_fma2(hb[1], make_float2(c0.x, c0.y), make_float2(d1.x, d1.y));
+        c_fma2(hb[2], make_float2(c1.x, c1.y), make_float2(d0.x, d0.y));
+        c_fma2(hb[3], make_float2(c1.x, c1.y), make_float2(d1.x, d1.y));
+        c_fma2(hb[0], make_float2(c0.z, c0.w), make_float2(d0.z, d0.w));
+        c_fma2(hb[1], make_float2(c0.z, c0.w), make_float2(d1.z, d1.w));
+        c_fma2(hb[2], make_float2(c1.z, c1.w), make_float2(d0.z, d0.w));
+        c_fma2(hb[3], make_float2(c1.z, c1.w), make_float2(d1.z, d1.w));
+      }
+      if (unb) {
+        const float sa0 = 1.f / (1.f - rho * ra0[ipa].x), sa1 = 1.f / (1.f - rho * ra1[ipa + hu].x);
+        const float sb0 = 1.f / (1.f - rho * rb0[ipb].x), sb1 = 1.f / (1.f - rho * rb1[ipb + hu].x);
+        ha[0] = c_scale(ha[0], sa0);
+        ha[1] = c_scale(ha[1], sa0);
+        ha[2] = c_scale(ha[2], sa1);
+        ha[3] = c_scale(ha[3], sa1);
+        hb[0] = c_scale(hb[0], sb0);
+        hb[1] = c_scale(hb[1], sb0);
+        hb[2] = c_scale(hb[2], sb1);
+        hb[3] = c_scale(hb[3], sb1);
+      }
       tm.sync();
-#pragma unroll
-      for (int k = 0; k < MAXE; ++k)
-        if (tid + k * NT < th * hu) put(tid + k * NT, hold[k][0], hold[k][1], hold[k][2], hold[k][3]);
+      if (live0) put(e0, ha[0], ha[1], ha[2], ha[3]);
+      if (e1 != e0) put(e1, hb[0], hb[1], hb[2], hb[3]);
     } else {
       for (int e = tid; e < th * hu; e += NT) {
         float2 c00, c01, c10, c11;
