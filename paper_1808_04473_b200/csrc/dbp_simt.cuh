@@ -370,11 +370,14 @@ __global__ void __launch_bounds__(NT, (UP == 64 ? (NT == 128 ? 4 : DBP_STATS64_M
       if (u == UP && !(reinterpret_cast<uintptr_t>(p.stats_in) & 15)) {  // float4 pairs, shifts instead of divisions
         constexpr int SH = (UP == 8) ? 2 : (UP == 16) ? 3 : (UP == 32) ? 4 : 5;  // log2(UP / 2)
         const float4* s4 = reinterpret_cast<const float4*>(src);  // rec is even: 16-byte aligned
+        // global -> shared without a register round trip (cp.async, 16 B each):
+        // every copy of the thread in flight at once, no registers held
         for (int e = tid; e < (UP * UP + T * UP) / 2; e += NT) {
           const int rr = e >> SH, cc = 2 * (e & (UP / 2 - 1));
           float2* dst = (rr < UP) ? w.G + rr * w.LD + cc : w.Z + (rr - UP) * w.LD + cc;
-          *reinterpret_cast<float4*>(dst) = s4[e];
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(s4 + e) : "memory");
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
       } else {
         for (int e = tid; e < u * u; e += NT) w.G[(e / u) * w.LD + (e % u)] = src[e];
         for (int e = tid; e < T * u; e += NT) w.Z[(e / u) * w.LD + (e % u)] = src[u * u + e];
